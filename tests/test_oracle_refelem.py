@@ -1,0 +1,145 @@
+"""Pins for the oracle's reference element and quadrature (CPU only).
+
+Every check compares against something other than the oracle's own formula:
+closed forms, paper/SPEC worked examples (tests/golden/paper_values.json),
+symmetry of the node set, or a second independent construction.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import exact, quadrature
+from oracle.refelem import RefElem, n_p
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+@pytest.mark.parametrize("npts", [1, 2, 3, 5, 8])
+def test_line_rule_moments(npts):
+    x, w = quadrature.line_rule(npts)
+    for k in range(2 * npts):
+        exact_m = 2.0 / (k + 1) if k % 2 == 0 else 0.0
+        assert abs(np.sum(w * x ** k) - exact_m) < 1e-14
+
+
+@pytest.mark.parametrize("npts", [1, 2, 4, 6, 9])
+def test_triangle_rule_moments(npts):
+    r, s, w = quadrature.triangle_rule(npts)
+    deg = 2 * npts - 1
+    for a in range(deg + 1):
+        for b in range(deg + 1 - a):
+            ref = float(exact.tri_moment(a, b))  # closed form, exact rational
+            assert abs(np.sum(w * r ** a * s ** b) - ref) < 1e-13, (a, b)
+
+
+def test_tri_moment_closed_form_bruteforce():
+    # brute force check of the closed form itself: 2-D midpoint sum on a fine grid
+    n = 400
+    h = 2.0 / n
+    c = -1 + h * (np.arange(n) + 0.5)
+    R, S = np.meshgrid(c, c)
+    inside = (R + S) <= 0
+    for a, b in [(0, 0), (1, 0), (0, 2), (2, 1), (3, 3)]:
+        approx = np.sum((R ** a * S ** b)[inside]) * h * h
+        assert abs(approx - float(exact.tri_moment(a, b))) < 2e-2
+    assert exact.tri_moment(0, 0) == Fraction(2)  # area of the bi-unit triangle
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_gll_closed_forms(N):
+    x = quadrature.jacobi_gl(0, 0, N)
+    ref = {2: [-1, 0, 1], 3: [-1, -GOLD["gll"]["N3_interior"], GOLD["gll"]["N3_interior"], 1],
+           4: [-1, -GOLD["gll"]["N4_interior"], 0, GOLD["gll"]["N4_interior"], 1]}[N]
+    assert np.allclose(x, ref, atol=1e-15)
+
+
+def test_nodes_low_degree_exact():
+    re1 = RefElem(1)
+    assert np.allclose(re1.r, [-1, 1, -1], atol=1e-15) and np.allclose(re1.s, [-1, -1, 1], atol=1e-15)
+    re2 = RefElem(2)
+    assert np.allclose(re2.r, GOLD["nodes_N2"]["r"], atol=1e-15)
+    assert np.allclose(re2.s, GOLD["nodes_N2"]["s"], atol=1e-15)
+    # N = 3: 9 edge nodes + the centroid (by the 3-fold symmetry)
+    re3 = RefElem(3)
+    interior = [(r, s) for r, s in zip(re3.r, re3.s) if r > -1 + 1e-9 and s > -1 + 1e-9 and r + s < -1e-9]
+    assert len(interior) == 1 and np.allclose(interior[0], (-1 / 3, -1 / 3), atol=1e-14)
+
+
+@pytest.mark.parametrize("N", range(1, 11))
+def test_node_set_invariants(N):
+    re = RefElem(N)
+    assert re.Np == n_p(N) == len(re.r)
+    assert np.all(re.r >= -1 - 1e-12) and np.all(re.s >= -1 - 1e-12) and np.all(re.r + re.s <= 1e-12)
+    assert re.Fmask.shape == (3, N + 1)
+    gll = quadrature.jacobi_gl(0, 0, N)
+    # face nodes sit at the GLL points, in the documented orientation
+    assert np.allclose(re.r[re.Fmask[0]], gll, atol=1e-13) and np.allclose(re.s[re.Fmask[0]], -1, atol=1e-13)
+    assert np.allclose(re.s[re.Fmask[1]], gll, atol=1e-13) and np.allclose(re.r[re.Fmask[1]], -gll, atol=1e-13)
+    assert np.allclose(re.s[re.Fmask[2]], gll, atol=1e-13) and np.allclose(re.r[re.Fmask[2]], -1, atol=1e-13)
+    # corners appear in exactly two face lists
+    cnt = np.bincount(re.Fmask.ravel(), minlength=re.Np)
+    assert sorted(np.nonzero(cnt == 2)[0].tolist()) == sorted([0, N, re.Np - 1])
+    assert np.linalg.cond(re.V) < 1e8
+    # the node set is invariant under the rotation of the triangle's vertices (barycentric cycle)
+    L = np.stack([-(re.r + re.s) / 2, (1 + re.r) / 2, (1 + re.s) / 2], 1)
+    rot = L[:, [1, 2, 0]]
+    r2, s2 = 2 * rot[:, 1] - 1, 2 * rot[:, 2] - 1
+    d = np.min(np.hypot(r2[:, None] - re.r[None, :], s2[:, None] - re.s[None, :]), axis=1)
+    assert d.max() < 1e-12
+
+
+@pytest.mark.parametrize("N", range(1, 11))
+def test_derivative_matrices_exact_on_polynomials(N):
+    re = RefElem(N)
+    r, s = re.r, re.s
+    for a in range(N + 1):
+        for b in range(N + 1 - a):
+            u = r ** a * s ** b
+            ur = a * r ** max(a - 1, 0) * s ** b if a else 0 * r
+            us = b * r ** a * s ** max(b - 1, 0) if b else 0 * r
+            assert np.abs(re.Dr @ u - ur).max() < 1e-10
+            assert np.abs(re.Ds @ u - us).max() < 1e-10
+
+
+def test_mass_N1_closed_form():
+    re = RefElem(1)
+    assert np.allclose(6 * re.M, GOLD["mass_N1"]["M_times_6"], atol=1e-14)
+    assert np.allclose(re.M.sum(axis=1), 2 / 3, atol=1e-14)
+
+
+@pytest.mark.parametrize("N", range(1, 9))
+def test_mass_by_quadrature_and_lift(N):
+    re = RefElem(N)
+    rq, sq, wq = quadrature.triangle_rule(N + 1)
+    V = re.eval_basis(rq, sq)
+    Mq = np.einsum("q,qi,qj->ij", wq, V, V)  # (l_i, l_j) by a rule pinned to closed-form moments
+    assert np.abs(Mq - re.M).max() < 1e-13
+    assert abs(re.M.sum() - 2.0) < 1e-13  # integral of 1 over the bi-unit triangle
+    assert np.all(np.linalg.eigvalsh(re.M) > 0)
+    # 1-D face mass by Gauss-Legendre on the face parameter
+    t, w = quadrature.line_rule(N + 1)
+    from oracle.refelem import vandermonde_1d
+    gll = quadrature.jacobi_gl(0, 0, N)
+    L = vandermonde_1d(N, t) @ np.linalg.inv(vandermonde_1d(N, gll))
+    assert np.abs(np.einsum("q,qi,qj->ij", w, L, L) - re.M1D).max() < 1e-13
+    assert abs(re.M1D.sum() - 2.0) < 1e-13
+    # Eq. elLift: M LIFT = E (face mass on the face rows)
+    assert np.abs(re.M @ re.LIFT - re.E).max() < 1e-12
+
+
+def test_m1d_N1_closed_form():
+    assert np.allclose(RefElem(1).M1D, [[2 / 3, 1 / 3], [1 / 3, 2 / 3]], atol=1e-15)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_exact_lagrange_basis_matches_float(N):
+    re = RefElem(N)
+    basis = exact.lagrange_basis(N)
+    for i, p in enumerate(basis):
+        vals = [float(sum(c * Fraction(r) ** a * Fraction(s) ** b for (a, b), c in p.items()))
+                for r, s in zip(re.r.tolist(), re.s.tolist())]
+        assert np.allclose(vals, np.eye(re.Np)[i], atol=1e-14)
