@@ -1,0 +1,196 @@
+"""B200-native FP64 SIPDG Poisson operator and Jacobi-PCG (arXiv:1801.00246 hot path).
+
+Thin Python layer over the C ABI of ``libipdg.so`` (include/ipdg.h).  Every
+step of the operator and the solver runs in the library's CUDA kernels; this
+module only marshals arguments.  PyTorch supplies device memory and streams
+(tensors are passed by ``data_ptr()``; the stream defaults to
+``torch.cuda.current_stream()``).  If the library is not built, calls raise.
+
+    import torch
+    from paper_1801_00246_b200 import Ipdg, meshgen
+    mesh = meshgen.square(316, jitter=0.2, diag="random", order="morton", seed=2)
+    op = Ipdg(N=4, mesh=mesh)
+    u = torch.rand(op.K, op.Np, dtype=torch.float64, device="cuda")
+    Au = op.ax(u)                                     # ipdg_ax
+    x, stats = op.pcg_solve(b, tol=1e-8, maxit=5000)  # ipdg_pcg_solve (Jacobi by default)
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib, meshgen  # noqa: F401
+from ._lib import IpdgError, check, ipdg_stats, lib  # noqa: F401
+
+__all__ = ["Ipdg", "IpdgError", "ipdg_stats", "lib", "meshgen"]
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Ipdg:
+    """One libipdg context (ipdg_create / ipdg_upload_mesh) bound to one CUDA device."""
+
+    def __init__(self, N, mesh=None, device=0, tau_scale=1.0):
+        self.N = int(N)
+        self.Np = (self.N + 1) * (self.N + 2) // 2
+        self.Nfp = self.N + 1
+        self.device = int(device)
+        self.ctx = ctypes.c_void_p()
+        check(lib().ipdg_create(ctypes.byref(self.ctx), self.N, self.device))
+        self.K = 0
+        self._ws = None
+        if mesh is not None:
+            self.upload_mesh(mesh, tau_scale)
+
+    def __del__(self):
+        try:
+            if self.ctx and self.ctx.value:
+                lib().ipdg_destroy(self.ctx)
+                self.ctx = ctypes.c_void_p()
+        except Exception:
+            pass
+
+    # ---- setup
+    def comm_init(self, nccl_id_bytes, nranks, rank):
+        buf = ctypes.create_string_buffer(bytes(nccl_id_bytes), len(nccl_id_bytes))
+        check(lib().ipdg_comm_init(self.ctx, buf, int(nranks), int(rank)), self.ctx)
+
+    def upload_mesh(self, mesh, tau_scale=1.0):
+        VX = np.ascontiguousarray(mesh["VX"], dtype=np.float64)
+        VY = np.ascontiguousarray(mesh["VY"], dtype=np.float64)
+        EToV = np.ascontiguousarray(mesh["EToV"], dtype=np.int32)
+        bc = np.ascontiguousarray(mesh["bc"], dtype=np.int8)
+        K = EToV.shape[0]
+        check(lib().ipdg_upload_mesh(self.ctx, K, VX.size, VX.ctypes.data, VY.ctypes.data, EToV.ctypes.data,
+                                     bc.ctypes.data, float(tau_scale)), self.ctx)
+        self.K = K
+        self._ws = None
+
+    def _workspace(self):
+        if self._ws is None:
+            import torch
+            n = ctypes.c_int64()
+            check(lib().ipdg_workspace_bytes(self.ctx, ctypes.byref(n)), self.ctx)
+            self._ws = torch.empty(n.value, dtype=torch.uint8, device="cuda:%d" % self.device)
+            check(lib().ipdg_set_workspace(self.ctx, _ptr(self._ws), n.value), self.ctx)
+        return self._ws
+
+    def _empty(self):
+        import torch
+        return torch.empty(self.K, self.Np, dtype=torch.float64, device="cuda:%d" % self.device)
+
+    # ---- operator
+    def ax(self, u, out=None, lam=0.0, stream=None):
+        out = self._empty() if out is None else out
+        check(lib().ipdg_ax(self.ctx, _ptr(u), _ptr(out), float(lam), _stream(stream)), self.ctx)
+        return out
+
+    def diag(self, lam=0.0, out=None, stream=None):
+        out = self._empty() if out is None else out
+        check(lib().ipdg_diag(self.ctx, _ptr(out), float(lam), _stream(stream)), self.ctx)
+        return out
+
+    def mass(self, u, out=None, stream=None):
+        out = self._empty() if out is None else out
+        check(lib().ipdg_mass(self.ctx, _ptr(u), _ptr(out), _stream(stream)), self.ctx)
+        return out
+
+    def nodes(self, stream=None):
+        x, y = self._empty(), self._empty()
+        check(lib().ipdg_nodes(self.ctx, _ptr(x), _ptr(y), _stream(stream)), self.ctx)
+        return x, y
+
+    # ---- solver
+    def pcg_solve(self, b, x=None, lam=0.0, precond=1, tol=1e-8, maxit=10000, stream=None):
+        self._workspace()
+        if x is None:
+            x = self._empty().zero_()
+        st = ipdg_stats()
+        rc = lib().ipdg_pcg_solve(self.ctx, _ptr(b), _ptr(x), float(lam), int(precond), float(tol), int(maxit),
+                                  ctypes.byref(st), _stream(stream))
+        check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
+        return x, dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+
+    def pcg_begin(self, b, x, lam=0.0, precond=1, tol=1e-8, stream=None):
+        self._workspace()
+        check(lib().ipdg_pcg_begin(self.ctx, _ptr(b), _ptr(x), float(lam), int(precond), float(tol),
+                                   _stream(stream)), self.ctx)
+
+    def pcg_iterate(self, n, stream=None):
+        check(lib().ipdg_pcg_iterate(self.ctx, int(n), _stream(stream)), self.ctx)
+
+    def pcg_iterate_profiled(self, n, stream=None):
+        """n iterations launched one by one with CUDA events around each pass: (ms_pass_a, ms_pass_b)."""
+        ta, tb = ctypes.c_double(), ctypes.c_double()
+        check(lib().ipdg_pcg_iterate_profiled(self.ctx, int(n), ctypes.byref(ta), ctypes.byref(tb), _stream(stream)),
+              self.ctx)
+        return ta.value, tb.value
+
+    def pcg_end(self, stream=None):
+        st = ipdg_stats()
+        rc = lib().ipdg_pcg_end(self.ctx, ctypes.byref(st), _stream(stream))
+        check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
+        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+
+    def pcg_solve_host(self, b_host, x_host, lam=0.0, precond=1, tol=1e-8, maxit=10000, stream=None):
+        """e2e path: host (pinned) numpy/torch CPU buffers in and out."""
+        st = ipdg_stats()
+        rc = lib().ipdg_pcg_solve_host(self.ctx, ctypes.c_void_p(b_host.data_ptr()), ctypes.c_void_p(x_host.data_ptr()),
+                                       float(lam), int(precond), float(tol), int(maxit), ctypes.byref(st),
+                                       _stream(stream))
+        check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
+        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+
+    # ---- introspection
+    def refop(self, name):
+        n = {"r": self.Np, "s": self.Np, "Dr": self.Np ** 2, "Ds": self.Np ** 2, "M": self.Np ** 2,
+             "M1D": self.Nfp ** 2, "LIFT": self.Np * 3 * self.Nfp, "Fmask": 3 * self.Nfp}[name]
+        buf = np.zeros(n)
+        got = lib().ipdg_get_refop(self.ctx, _lib.OPS[name], buf.ctypes.data, n)
+        if got != n:
+            check(got if got < 0 else _lib.IPDG_EINVAL, self.ctx)
+        shape = {"Dr": (self.Np, self.Np), "Ds": (self.Np, self.Np), "M": (self.Np, self.Np),
+                 "M1D": (self.Nfp, self.Nfp), "LIFT": (self.Np, 3 * self.Nfp), "Fmask": (3, self.Nfp)}.get(name)
+        return buf.reshape(shape) if shape else buf
+
+    def geofacs(self):
+        buf = np.zeros(self.K * 5)
+        check(lib().ipdg_get_geofacs(self.ctx, buf.ctypes.data, buf.size), self.ctx)
+        return buf.reshape(self.K, 5)
+
+    def connectivity(self):
+        e = np.zeros(self.K * 3, dtype=np.int32)
+        f = np.zeros(self.K * 3, dtype=np.int32)
+        check(lib().ipdg_get_connectivity(self.ctx, e.ctypes.data, f.ctypes.data, e.size), self.ctx)
+        return e.reshape(self.K, 3), f.reshape(self.K, 3)
+
+    def info(self):
+        out = (ctypes.c_int64 * 8)()
+        check(lib().ipdg_info(self.ctx, out, 8), self.ctx)
+        keys = ["N", "Np", "K", "nblocks", "E", "gmax", "smem_bytes", "grid"]
+        return dict(zip(keys, list(out)))
+
+    def launch_count(self):
+        return int(lib().ipdg_launch_count(self.ctx))
+
+
+def nccl_unique_id():
+    n = lib().ipdg_nccl_id_bytes()
+    buf = ctypes.create_string_buffer(n)
+    check(lib().ipdg_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+# expose the C names (same names as include/ipdg.h) for direct use
+def __getattr__(name):
+    if name.startswith("ipdg_") and name in _lib.SIGNATURES:
+        return getattr(lib(), name)
+    raise AttributeError(name)

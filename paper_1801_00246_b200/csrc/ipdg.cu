@@ -1,0 +1,1004 @@
+// libipdg: C ABI (include/ipdg.h) over the sm_100a SIPDG kernels.
+// Paper: arXiv:1801.00246 (P:n = PAPER.md line n).  Design: DESIGN.md.
+//
+// Host responsibilities (setup, once per mesh): reference operators (refops.cpp),
+// face connectivity by vertex-pair matching, the element-block schedule with its
+// ghost lists, DMMA fragment tables, geometric factors (on the device), the Jacobi
+// diagonal.  Hot path (every call): k_sipdg (Ax, or PCG pass A fused with the
+// direction update and p.Ap), k_pcg_b (residual update fused with r.z and r.r),
+// all on the caller's stream; PCG iterations are replayed from captured CUDA graphs.
+//
+// PCG protocol (device-resident scalars, PcgState):
+//   begin:  Ap = A x0;  r = b - Ap;  red_B = (r.z, r.r, b.b)       [+ allreduce(3)]
+//   iter k: pass A (k_sipdg MODE_PCG_A): decide stop from red_B (rr_{k-1} <= tol^2 bb,
+//             or k-1 = maxit); else beta = rho_{k-1}/rho_{k-2}; p_k = D^-1 r + beta p_{k-1}
+//             (double-buffered); x += alpha_{k-1} p_{k-1} (deferred); Ap = A p_k;
+//             red_A = p_k . Ap                                          [+ allreduce(1)]
+//           pass B (k_pcg_b): alpha_k = rho_{k-1}/red_A (breakdown if <= 0);
+//             r -= alpha_k Ap; red_B = (r.z, r.r); it = k               [+ allreduce(2)]
+//   end:    pending x += alpha_k p_k if no stop was decided; stats to host.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/ipdg.h"
+#include "refops.h"
+#include "sipdg_kernels.cuh"
+
+using namespace ipdg;
+
+struct ipdg_ctx_s {
+  int N = 0, device = 0, sms = 0;
+  RefOps ref;
+  int64_t K = 0, H = 0;  // local elements, halo ghosts
+  double tau_c = 0.0;
+  bool has_dirichlet = false;
+  // device mesh data
+  double4* geo = nullptr;
+  short4* nbr = nullptr;
+  int* goff = nullptr;
+  int* gid = nullptr;
+  int* boff = nullptr;
+  int* etoe = nullptr;
+  int8_t* bcode = nullptr;
+  double* vxy = nullptr;
+  double* rs = nullptr;
+  double* Mref = nullptr;
+  double* tables = nullptr;
+  double* diagtab = nullptr;
+  int nblocks = 0, gmax = 0;
+  int E = 0;
+  size_t smem[2] = {0, 0};
+  int grid[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
+  // host copies for introspection
+  std::vector<int> etoe_h, etof_h;
+  // PCG
+  PcgState* st = nullptr;
+  PcgState* st_host = nullptr;
+  double* partials = nullptr;
+  unsigned int* counter = nullptr;
+  void* ws = nullptr;
+  int64_t ws_bytes = 0;
+  bool ws_owned = false;
+  double *r = nullptr, *pe = nullptr, *po = nullptr, *Ap = nullptr, *dinv = nullptr;
+  double dinv_lambda = -1.0;
+  bool dinv_valid = false;
+  // current solve
+  double* x = nullptr;
+  double lambda = 0.0;
+  int precond = 0;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0]: 1 iteration, [1]: kChunk iterations
+  const void* gkey_x = nullptr;
+  double gkey_lambda = -1.0;
+  int gkey_precond = -1;
+  cudaStream_t cap_stream = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::string err;
+  int64_t launches = 0;
+};
+
+static constexpr int kChunk = 32;
+
+#define FAIL(ctx, code, ...)                                         \
+  do {                                                              \
+    char b_[512];                                                   \
+    snprintf(b_, sizeof(b_), __VA_ARGS__);                          \
+    if (ctx) (ctx)->err = b_;                                        \
+    return code;                                                    \
+  } while (0)
+#define CUDA_TRY(ctx, x)                                                                            \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess) FAIL(ctx, IPDG_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define NCCL_TRY(ctx, x)                                                                           \
+  do {                                                                                             \
+    ncclResult_t r_ = (x);                                                                         \
+    if (r_ != ncclSuccess) FAIL(ctx, IPDG_ENCCL, "%s: %s", #x, ncclGetErrorString(r_));            \
+  } while (0)
+
+// ------------------------------------------------------------------ per-N dispatch
+template <int N>
+struct Impl {
+  using T = Tr<N>;
+
+  // DMMA fragment tables: [chunk][ntile][lane], lane -> (k = lane & 3, n = lane >> 2)
+  static std::vector<double> build_tables(const RefOps& R) {
+    const int NP = T::NP, NFP = T::NFP, NF3 = T::NF3, NT = T::NT;
+    std::vector<double> tab(T::TAB_G + T::TAB_M + T::TAB_L, 0.0);
+    double* tg = tab.data();
+    double* tm = tg + T::TAB_G;
+    double* tl = tm + T::TAB_M;
+    auto at = [&](const std::vector<double>& A, int ld, int i, int j, int ni, int nj) {
+      return (i < ni && j < nj) ? A[i * ld + j] : 0.0;
+    };
+    for (int kc = 0; kc < T::KCG; ++kc)
+      for (int q = 0; q < 2 * NT; ++q)
+        for (int l = 0; l < 32; ++l) {
+          const int k = 4 * kc + (l & 3), n = 8 * (q % NT) + (l >> 2);
+          const std::vector<double>& D = (q < NT) ? R.Dr : R.Ds;
+          tg[(kc * 2 * NT + q) * 32 + l] = at(D, NP, n, k, NP, NP);  // B[k][n] = D[n][k]
+        }
+    // LIFT^T Sr, LIFT^T Ss  (3Nfp x Np)
+    std::vector<double> LSr(NF3 * NP, 0.0), LSs(NF3 * NP, 0.0);
+    for (int m = 0; m < NF3; ++m)
+      for (int n = 0; n < NP; ++n) {
+        double a = 0, b = 0;
+        for (int i = 0; i < NP; ++i) {
+          a += R.LIFT[i * NF3 + m] * R.Sr[i * NP + n];
+          b += R.LIFT[i * NF3 + m] * R.Ss[i * NP + n];
+        }
+        LSr[m * NP + n] = a;
+        LSs[m * NP + n] = b;
+      }
+    for (int c = 0; c < T::KCW + T::KCF; ++c)
+      for (int j = 0; j < NT; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int n = 8 * j + (l >> 2);
+          double v = 0.0;
+          if (c < 4 * NT) {  // w_r / w_s chunks straight from the C-fragment layout
+            const int cc = c % (2 * NT);
+            const int i = 8 * (cc >> 1) + 2 * (l & 3) + (cc & 1);
+            v = at(c < 2 * NT ? R.Sr : R.Ss, NP, i, n, NP, NP);
+          } else {
+            const int m = 4 * (c - 4 * NT) + (l & 3);
+            if (m < NF3) v = at(LSr, NP, m, n, NF3, NP);
+            else if (m < 2 * NF3) v = at(LSs, NP, m - NF3, n, NF3, NP);
+          }
+          tm[(c * NT + j) * 32 + l] = v;
+        }
+    for (int kc = 0; kc < T::KCM; ++kc)
+      for (int j = 0; j < NT; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int k = 4 * kc + (l & 3), n = 8 * j + (l >> 2);
+          tl[(kc * NT + j) * 32 + l] = at(R.M, NP, k, n, NP, NP);
+        }
+    // aux: M1D, then ints fmask[NF3], nodeface[2*NPN]
+    for (int i = 0; i < NFP * NFP; ++i) tab.push_back(R.M1D[i]);
+    std::vector<int> ia(NF3 + 2 * T::NPN, -1);
+    for (int i = 0; i < NF3; ++i) ia[i] = R.Fmask[i];
+    for (int f = 0; f < 3; ++f)
+      for (int k = 0; k < NFP; ++k) {
+        const int i = R.Fmask[f * NFP + k];
+        int* slot = &ia[NF3 + 2 * i];
+        if (slot[0] < 0) slot[0] = f * NFP + k;
+        else slot[1] = f * NFP + k;
+      }
+    if (ia.size() % 2) ia.push_back(-1);
+    const size_t base = tab.size();
+    tab.resize(base + ia.size() / 2);
+    std::memcpy(tab.data() + base, ia.data(), ia.size() * sizeof(int));
+    return tab;
+  }
+
+  static std::vector<double> build_diagtab(const RefOps& R) {
+    const int NP = T::NP, NFP = T::NFP, NF3 = T::NF3;
+    std::vector<double> d(4 * NP + 2 * NF3 + NFP + NF3, 0.0);
+    for (int i = 0; i < NP; ++i) {
+      double krr = 0, krs = 0, kss = 0;
+      for (int a = 0; a < NP; ++a)
+        for (int b = 0; b < NP; ++b) {
+          const double m = R.M[a * NP + b];
+          krr += R.Dr[a * NP + i] * m * R.Dr[b * NP + i];
+          krs += R.Dr[a * NP + i] * m * R.Ds[b * NP + i];
+          kss += R.Ds[a * NP + i] * m * R.Ds[b * NP + i];
+        }
+      d[i] = krr;
+      d[NP + i] = krs;
+      d[2 * NP + i] = kss;
+      d[3 * NP + i] = R.M[i * NP + i];
+    }
+    for (int f = 0; f < 3; ++f)
+      for (int k = 0; k < NFP; ++k) {
+        const int i = R.Fmask[f * NFP + k];
+        double pr = 0, ps = 0;
+        for (int m = 0; m < NFP; ++m) {
+          const int fm = R.Fmask[f * NFP + m];
+          pr += R.Dr[fm * NP + i] * R.M1D[m * NFP + k];
+          ps += R.Ds[fm * NP + i] * R.M1D[m * NFP + k];
+        }
+        d[4 * NP + f * NFP + k] = pr;
+        d[4 * NP + NF3 + f * NFP + k] = ps;
+      }
+    for (int k = 0; k < NFP; ++k) d[4 * NP + 2 * NF3 + k] = R.M1D[k * NFP + k];
+    for (int i = 0; i < NF3; ++i) d[4 * NP + 2 * NF3 + NFP + i] = R.Fmask[i];
+    return d;
+  }
+
+  static int configure(ipdg_ctx c) {
+    for (int lam = 0; lam < 2; ++lam) {
+      const SmemLayout L = SmemLayout::make<N>(c->gmax, lam != 0);
+      const size_t bytes = (size_t)L.total * sizeof(double);
+      c->smem[lam] = bytes;
+      for (int mode = 0; mode < 2; ++mode) {
+        const void* fn = (mode == 0) ? (lam ? (const void*)k_sipdg<N, MODE_AX, true> : (const void*)k_sipdg<N, MODE_AX, false>)
+                                     : (lam ? (const void*)k_sipdg<N, MODE_PCG_A, true>
+                                            : (const void*)k_sipdg<N, MODE_PCG_A, false>);
+        // opt in to the full per-CTA maximum once: the attribute is per function (shared by all
+        // contexts of this N), the launch passes the context's own byte count
+        int optin = 0;
+        CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        if ((int)bytes > optin - 1024) FAIL(c, IPDG_ECUDA, "k_sipdg<N=%d> needs %zu B of shared memory", N, bytes);
+        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        int occ = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
+        if (occ < 1) FAIL(c, IPDG_ECUDA, "k_sipdg<N=%d> does not fit on an SM (smem %zu B, gmax %d)", N, bytes, c->gmax);
+        c->grid[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
+      }
+    }
+    return IPDG_OK;
+  }
+
+  static AxArgs args(ipdg_ctx c) {
+    AxArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.K = c->K;
+    a.nblocks = c->nblocks;
+    a.geo = c->geo;
+    a.nbr = c->nbr;
+    a.goff = c->goff;
+    a.gid = c->gid;
+    a.boff = c->boff;
+    a.tables = c->tables;
+    a.tau_c = c->tau_c;
+    return a;
+  }
+
+  static int ax(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
+    AxArgs a = args(c);
+    a.u = u;
+    a.Au = Au;
+    a.lambda = lambda;
+    const bool lam = lambda != 0.0;
+    const int g = c->grid[0][lam];
+    if (lam) k_sipdg<N, MODE_AX, true><<<g, T::W * 32, c->smem[1], s>>>(a, c->gmax);
+    else k_sipdg<N, MODE_AX, false><<<g, T::W * 32, c->smem[0], s>>>(a, c->gmax);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
+  static int pass_a(ipdg_ctx c, cudaStream_t s) {
+    AxArgs a = args(c);
+    a.lambda = c->lambda;
+    a.r = c->r;
+    a.dinv = c->precond ? c->dinv : nullptr;
+    a.p_even = c->pe;
+    a.p_odd = c->po;
+    a.x = c->x;
+    a.Au = c->Ap;
+    a.st = c->st;
+    a.partials = c->partials;
+    a.counter = c->counter;
+    const bool lam = c->lambda != 0.0;
+    const int g = c->grid[1][lam];
+    if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1], s>>>(a, c->gmax);
+    else k_sipdg<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem[0], s>>>(a, c->gmax);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
+  static int diag(ipdg_ctx c, double* d, double lambda, cudaStream_t s) {
+    const int64_t n = c->K * T::NP;
+    k_diag<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->etoe, c->bcode, c->diagtab, c->tau_c, lambda, d);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
+  static int mass(ipdg_ctx c, const double* u, double* Mu, cudaStream_t s) {
+    const int64_t n = c->K * T::NP;
+    k_mass<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->Mref, u, Mu);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+};
+
+#define DISPATCH(N_, CALL)                     \
+  switch (N_) {                                \
+    case 1: return Impl<1>::CALL;              \
+    case 2: return Impl<2>::CALL;              \
+    case 3: return Impl<3>::CALL;              \
+    case 4: return Impl<4>::CALL;              \
+    case 5: return Impl<5>::CALL;              \
+    case 6: return Impl<6>::CALL;              \
+    case 7: return Impl<7>::CALL;              \
+    case 8: return Impl<8>::CALL;              \
+    default: return IPDG_EDEGREE;              \
+  }
+
+static int e_of(int N) {
+  switch (N) {
+    case 1: return Tr<1>::E; case 2: return Tr<2>::E; case 3: return Tr<3>::E; case 4: return Tr<4>::E;
+    case 5: return Tr<5>::E; case 6: return Tr<6>::E; case 7: return Tr<7>::E; default: return Tr<8>::E;
+  }
+}
+static std::vector<double> tables_of(const RefOps& R) {
+  switch (R.N) {
+    case 1: return Impl<1>::build_tables(R); case 2: return Impl<2>::build_tables(R);
+    case 3: return Impl<3>::build_tables(R); case 4: return Impl<4>::build_tables(R);
+    case 5: return Impl<5>::build_tables(R); case 6: return Impl<6>::build_tables(R);
+    case 7: return Impl<7>::build_tables(R); default: return Impl<8>::build_tables(R);
+  }
+}
+static std::vector<double> diagtab_of(const RefOps& R) {
+  switch (R.N) {
+    case 1: return Impl<1>::build_diagtab(R); case 2: return Impl<2>::build_diagtab(R);
+    case 3: return Impl<3>::build_diagtab(R); case 4: return Impl<4>::build_diagtab(R);
+    case 5: return Impl<5>::build_diagtab(R); case 6: return Impl<6>::build_diagtab(R);
+    case 7: return Impl<7>::build_diagtab(R); default: return Impl<8>::build_diagtab(R);
+  }
+}
+
+// largest ghost count per block that keeps k_sipdg<N> (lambda variant) within the SM's
+// opt-in shared memory at one CTA per SM
+template <int N>
+static int ghost_cap_n(int device) {
+  using T = Tr<N>;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (optin <= 0) optin = 227 * 1024;
+  const int fixed = SmemLayout::make<N>(0, true).total * 8 + 1024;  // + static smem
+  const int per = (T::SU + T::NF3 + 5) * 8;
+  int g = (optin - fixed) / per;
+  g = g / 8 * 8;
+  return std::max(8, std::min(g, 30000 - T::E));
+}
+static int ghost_cap(int N, int device) {
+  switch (N) {
+    case 1: return ghost_cap_n<1>(device); case 2: return ghost_cap_n<2>(device);
+    case 3: return ghost_cap_n<3>(device); case 4: return ghost_cap_n<4>(device);
+    case 5: return ghost_cap_n<5>(device); case 6: return ghost_cap_n<6>(device);
+    case 7: return ghost_cap_n<7>(device); default: return ghost_cap_n<8>(device);
+  }
+}
+
+template <class Tp>
+static int upload(ipdg_ctx c, Tp** dst, const Tp* src, size_t n) {
+  if (*dst) cudaFree(*dst);
+  *dst = nullptr;
+  CUDA_TRY(c, cudaMalloc((void**)dst, std::max<size_t>(n, 1) * sizeof(Tp)));
+  if (n) CUDA_TRY(c, cudaMemcpy(*dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice));
+  return IPDG_OK;
+}
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != IPDG_OK) return rc_; \
+  } while (0)
+
+static void free_mesh(ipdg_ctx c) {
+  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  c->geo = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
+  c->bcode = nullptr;
+  c->vxy = nullptr;
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->gkey_x = nullptr;
+  c->dinv_valid = false;
+}
+
+static void free_ws(ipdg_ctx c) {
+  if (c->ws_owned && c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  c->ws_owned = false;
+  c->ws_bytes = 0;
+  c->r = c->pe = c->po = c->Ap = c->dinv = nullptr;
+  c->dinv_valid = false;
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->gkey_x = nullptr;
+}
+
+extern "C" {
+
+const char* ipdg_strerror(int code) {
+  switch (code) {
+    case IPDG_OK: return "ok";
+    case IPDG_NOT_CONVERGED: return "not converged (maxit reached)";
+    case IPDG_EINVAL: return "invalid argument";
+    case IPDG_EDEGREE: return "degree N out of range 1..8";
+    case IPDG_EMESH: return "invalid mesh";
+    case IPDG_EBREAKDOWN: return "PCG breakdown (p^T A p <= 0)";
+    case IPDG_ESINGULAR: return "singular operator (lambda = 0 and no Dirichlet face)";
+    case IPDG_ECUDA: return "CUDA error";
+    case IPDG_ENCCL: return "NCCL error";
+    case IPDG_ESTATE: return "invalid call order";
+    default: return "unknown error";
+  }
+}
+
+int ipdg_last_error(ipdg_ctx c, char* buf, int cap) {
+  if (!c || !buf || cap <= 0) return IPDG_EINVAL;
+  snprintf(buf, cap, "%s", c->err.c_str());
+  return IPDG_OK;
+}
+
+int ipdg_create(ipdg_ctx* out, int N, int device) {
+  if (!out) return IPDG_EINVAL;
+  *out = nullptr;
+  if (N < 1 || N > 8) return IPDG_EDEGREE;
+  ipdg_ctx c = new ipdg_ctx_s();
+  c->N = N;
+  c->device = device;
+  c->E = e_of(N);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return IPDG_ECUDA;
+  }
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  try {
+    c->ref = build_refops(N);
+  } catch (const std::exception& e) {
+    delete c;
+    return IPDG_ECUDA;
+  }
+  const RefOps& R = c->ref;
+  int rc = IPDG_OK;
+  std::vector<double> tab = tables_of(R), dtab = diagtab_of(R), rs(2 * R.Np);
+  for (int i = 0; i < R.Np; ++i) { rs[i] = R.r[i]; rs[R.Np + i] = R.s[i]; }
+  if ((rc = upload(c, &c->tables, tab.data(), tab.size())) || (rc = upload(c, &c->diagtab, dtab.data(), dtab.size())) ||
+      (rc = upload(c, &c->rs, rs.data(), rs.size())) || (rc = upload(c, &c->Mref, R.M.data(), R.M.size()))) {
+    delete c;
+    return rc;
+  }
+  if (cudaMalloc(&c->st, sizeof(PcgState)) != cudaSuccess || cudaMallocHost(&c->st_host, sizeof(PcgState)) != cudaSuccess ||
+      cudaMalloc(&c->counter, sizeof(unsigned int)) != cudaSuccess || cudaMemset(c->counter, 0, sizeof(unsigned int)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return IPDG_ECUDA;
+  }
+  *out = c;
+  return IPDG_OK;
+}
+
+int ipdg_destroy(ipdg_ctx c) {
+  if (!c) return IPDG_EINVAL;
+  cudaSetDevice(c->device);
+  free_mesh(c);
+  free_ws(c);
+  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->st, c->counter, c->partials};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return IPDG_OK;
+}
+
+int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const double* VY, const int32_t* EToV,
+                     const int8_t* bc, double tau_scale) {
+  if (!c) return IPDG_EINVAL;
+  if (K <= 0 || Nv <= 0 || !VX || !VY || !EToV || !bc || !(tau_scale > 0.0))
+    FAIL(c, IPDG_EINVAL, "upload_mesh: bad arguments");
+  if (K > (int64_t)INT32_MAX / 3) FAIL(c, IPDG_EINVAL, "upload_mesh: K too large");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  free_mesh(c);
+  const int E = c->E;
+  // ---- connectivity by sorting vertex-pair keys
+  std::vector<std::pair<uint64_t, int64_t>> keys((size_t)K * 3);
+  for (int64_t e = 0; e < K; ++e)
+    for (int f = 0; f < 3; ++f) {
+      const int64_t a = EToV[e * 3 + f], b = EToV[e * 3 + (f + 1) % 3];
+      if (a < 0 || b < 0 || a >= Nv || b >= Nv || a == b) FAIL(c, IPDG_EMESH, "element %lld has an invalid vertex id", (long long)e);
+      if (bc[e * 3 + f] < 0 || bc[e * 3 + f] > 3) FAIL(c, IPDG_EINVAL, "element %lld face %d: bad boundary code", (long long)e, f);
+      keys[e * 3 + f] = {(uint64_t)std::min(a, b) * (uint64_t)Nv + (uint64_t)std::max(a, b), e * 3 + f};
+    }
+  std::sort(keys.begin(), keys.end());
+  std::vector<int> etoe(K * 3, -1), etof(K * 3, -1);
+  for (size_t i = 0; i < keys.size();) {
+    size_t j = i + 1;
+    while (j < keys.size() && keys[j].first == keys[i].first) ++j;
+    if (j - i > 2) FAIL(c, IPDG_EMESH, "non-manifold edge (face id %lld)", (long long)keys[i].second);
+    if (j - i == 2) {
+      const int64_t a = keys[i].second, b = keys[i + 1].second;
+      etoe[a] = (int)(b / 3); etof[a] = (int)(b % 3);
+      etoe[b] = (int)(a / 3); etof[b] = (int)(a % 3);
+    }
+    i = j;
+  }
+  bool dir = false;
+  for (int64_t i = 0; i < K * 3; ++i) {
+    if (bc[i] == IPDG_BC_INTERIOR && etoe[i] < 0) FAIL(c, IPDG_EMESH, "interior face (%lld,%lld) has no neighbour", (long long)(i / 3), (long long)(i % 3));
+    if (bc[i] != IPDG_BC_INTERIOR && etoe[i] >= 0) FAIL(c, IPDG_EMESH, "boundary-coded face (%lld,%lld) has a neighbour", (long long)(i / 3), (long long)(i % 3));
+    if (bc[i] == IPDG_BC_REMOTE) FAIL(c, IPDG_EINVAL, "remote faces need ipdg_comm_init (multi-GPU)");
+    if (bc[i] == IPDG_BC_DIRICHLET) dir = true;
+  }
+  c->has_dirichlet = dir;
+  // ---- element blocks and ghost lists.  A block is a contiguous range of at most E own
+  // elements whose distinct outside face neighbours (ghosts) fit the shared-memory budget
+  // gcap; well-ordered meshes (Morton, RCB) never hit the cap, scattered orderings get
+  // shorter blocks instead of failing.
+  const int gcap = ghost_cap(c->N, c->sms > 0 ? c->device : 0);
+  std::vector<int> goff(1, 0), gid, boff(1, 0);
+  std::vector<short4> nbr(K);
+  int gmax = 0;
+  std::vector<int> gl;
+  int64_t e0 = 0;
+  while (e0 < K) {
+    // grow the block greedily
+    gl.clear();
+    int64_t e1 = e0;
+    while (e1 < K && e1 - e0 < E) {
+      size_t before = gl.size();
+      for (int f = 0; f < 3; ++f) {
+        const int n = etoe[e1 * 3 + f];
+        if (n >= 0 && (n < e0 || n > e1)) gl.push_back(n);
+      }
+      std::sort(gl.begin(), gl.end());
+      gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+      // neighbours inside [e0, e1] are own elements: drop them from the ghost list
+      gl.erase(std::remove_if(gl.begin(), gl.end(), [&](int n) { return n >= e0 && n <= e1; }), gl.end());
+      if ((int)gl.size() > gcap && e1 > e0) {  // roll back this element
+        gl.resize(before);
+        gl.clear();
+        for (int64_t e = e0; e < e1; ++e)
+          for (int f = 0; f < 3; ++f) {
+            const int n = etoe[e * 3 + f];
+            if (n >= 0 && (n < e0 || n >= e1)) gl.push_back(n);
+          }
+        std::sort(gl.begin(), gl.end());
+        gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+        break;
+      }
+      ++e1;
+    }
+    gmax = std::max<int>(gmax, (int)gl.size());
+    for (int64_t e = e0; e < e1; ++e) {
+      short sl[3] = {0, 0, 0};
+      int flags = 0;
+      for (int f = 0; f < 3; ++f) {
+        const int n = etoe[e * 3 + f];
+        int slot = 0;
+        if (n >= 0) {
+          if (n >= e0 && n < e1) slot = (int)(n - e0);
+          else slot = E + (int)(std::lower_bound(gl.begin(), gl.end(), n) - gl.begin());
+        }
+        sl[f] = (short)slot;
+        const int fp = n >= 0 ? etof[e * 3 + f] : 0;
+        flags |= ((fp & 3) | ((bc[e * 3 + f] & 3) << 2)) << (4 * f);
+      }
+      nbr[e] = make_short4(sl[0], sl[1], sl[2], (short)flags);
+    }
+    gid.insert(gid.end(), gl.begin(), gl.end());
+    goff.push_back((int)gid.size());
+    boff.push_back((int)e1);
+    e0 = e1;
+  }
+  const int nb = (int)boff.size() - 1;
+  if (E + gmax > 32000) FAIL(c, IPDG_EMESH, "element ordering too scattered (a block has %d ghosts)", gmax);
+  c->K = K;
+  c->nblocks = nb;
+  c->gmax = gmax;
+  c->tau_c = 0.5 * (c->N + 1) * (c->N + 2) * tau_scale;
+  std::vector<double> vxy(K * 6);
+  for (int64_t e = 0; e < K; ++e)
+    for (int v = 0; v < 3; ++v) {
+      vxy[e * 6 + 2 * v] = VX[EToV[e * 3 + v]];
+      vxy[e * 6 + 2 * v + 1] = VY[EToV[e * 3 + v]];
+    }
+  std::vector<int8_t> bcv(bc, bc + K * 3);
+  TRY(upload(c, &c->vxy, vxy.data(), vxy.size()));
+  TRY(upload(c, &c->nbr, nbr.data(), nbr.size()));
+  TRY(upload(c, &c->goff, goff.data(), goff.size()));
+  TRY(upload(c, &c->gid, gid.data(), gid.size()));
+  TRY(upload(c, &c->boff, boff.data(), boff.size()));
+  TRY(upload(c, &c->etoe, etoe.data(), etoe.size()));
+  TRY(upload(c, &c->bcode, bcv.data(), bcv.size()));
+  c->etoe_h = etoe;
+  c->etof_h = etof;
+  CUDA_TRY(c, cudaMalloc(&c->geo, K * sizeof(double4)));
+  unsigned long long* bad = nullptr;
+  CUDA_TRY(c, cudaMalloc(&bad, sizeof(unsigned long long)));
+  const unsigned long long none = ~0ull;
+  CUDA_TRY(c, cudaMemcpy(bad, &none, sizeof(none), cudaMemcpyHostToDevice));
+  k_geometry<<<(unsigned)((K + 255) / 256), 256>>>(K, c->vxy, c->geo, bad);
+  c->launches++;
+  unsigned long long badh = none;
+  CUDA_TRY(c, cudaMemcpy(&badh, bad, sizeof(badh), cudaMemcpyDeviceToHost));
+  cudaFree(bad);
+  if (badh != none) FAIL(c, IPDG_EMESH, "element %llu has J <= 0 (vertices must be counter-clockwise)", badh);
+  DISPATCH(c->N, configure(c));
+}
+
+int ipdg_ax(ipdg_ctx c, const double* u, double* Au, double lambda, void* stream) {
+  if (!c || !u || !Au || u == Au || !(lambda >= 0.0)) return c ? (c->err = "ipdg_ax: bad arguments", IPDG_EINVAL) : IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_ax before ipdg_upload_mesh");
+  DISPATCH(c->N, ax(c, u, Au, lambda, (cudaStream_t)stream));
+}
+
+int ipdg_diag(ipdg_ctx c, double* d, double lambda, void* stream) {
+  if (!c || !d || !(lambda >= 0.0)) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_diag before ipdg_upload_mesh");
+  DISPATCH(c->N, diag(c, d, lambda, (cudaStream_t)stream));
+}
+
+int ipdg_mass(ipdg_ctx c, const double* u, double* Mu, void* stream) {
+  if (!c || !u || !Mu || u == Mu) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_mass before ipdg_upload_mesh");
+  DISPATCH(c->N, mass(c, u, Mu, (cudaStream_t)stream));
+}
+
+int ipdg_nodes(ipdg_ctx c, double* x, double* y, void* stream) {
+  if (!c || !x || !y) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_nodes before ipdg_upload_mesh");
+  const int64_t n = c->K * c->ref.Np;
+  k_nodes<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(c->K, c->ref.Np, c->vxy, c->rs, x, y);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+int ipdg_workspace_bytes(ipdg_ctx c, int64_t* bytes) {
+  if (!c || !bytes) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "workspace size needs a mesh");
+  const int64_t n = (c->K + c->H) * c->ref.Np;
+  *bytes = 5 * ((n * 8 + 255) / 256 * 256);
+  return IPDG_OK;
+}
+
+static int bind_ws(ipdg_ctx c) {
+  const int64_t n = (c->K + c->H) * c->ref.Np;
+  const int64_t seg = (n * 8 + 255) / 256 * 256;
+  char* b = (char*)c->ws;
+  c->r = (double*)(b);
+  c->pe = (double*)(b + seg);
+  c->po = (double*)(b + 2 * seg);
+  c->Ap = (double*)(b + 3 * seg);
+  c->dinv = (double*)(b + 4 * seg);
+  c->dinv_valid = false;
+  return IPDG_OK;
+}
+
+int ipdg_set_workspace(ipdg_ctx c, void* dev, int64_t bytes) {
+  if (!c || !dev) return IPDG_EINVAL;
+  int64_t need = 0;
+  TRY(ipdg_workspace_bytes(c, &need));
+  if (bytes < need) FAIL(c, IPDG_EINVAL, "workspace too small: %lld < %lld", (long long)bytes, (long long)need);
+  if (c->ws == dev && !c->ws_owned) return IPDG_OK;
+  free_ws(c);
+  c->ws = dev;
+  c->ws_bytes = bytes;
+  c->ws_owned = false;
+  return bind_ws(c);
+}
+
+static int ensure_ws(ipdg_ctx c) {
+  if (c->ws) return IPDG_OK;
+  int64_t need = 0;
+  TRY(ipdg_workspace_bytes(c, &need));
+  CUDA_TRY(c, cudaMalloc(&c->ws, need));
+  c->ws_owned = true;
+  c->ws_bytes = need;
+  return bind_ws(c);
+}
+
+static int ensure_partials(ipdg_ctx c) {
+  if (c->partials) return IPDG_OK;
+  CUDA_TRY(c, cudaMalloc(&c->partials, 3 * sizeof(double) * std::max(4096, 4 * c->sms * 16)));
+  return IPDG_OK;
+}
+
+__global__ void k_recip(int64_t n, double* d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) d[i] = 1.0 / d[i];
+}
+
+static int allreduce(ipdg_ctx c, double* buf, int n, cudaStream_t s) {
+  if (c->comm && c->nranks > 1) NCCL_TRY(c, ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, c->comm, s));
+  return IPDG_OK;
+}
+
+static int vec_grid(ipdg_ctx c) { return std::min(c->sms * 8, 4096); }
+
+static int one_iteration(ipdg_ctx c, cudaStream_t s) {
+  TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
+  TRY(allreduce(c, &c->st->red_A, 1, s));
+  k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->st,
+                                        c->partials, c->counter);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  TRY(allreduce(c, c->st->red_B, 2, s));
+  return IPDG_OK;
+}
+
+static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = IPDG_OK;
+  for (int i = 0; i < iters && rc == IPDG_OK; ++i) rc = one_iteration(c, c->cap_stream);
+  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+  if (rc != IPDG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) FAIL(c, IPDG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) FAIL(c, IPDG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  return IPDG_OK;
+}
+
+int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, void* stream) {
+  if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || (precond != 0 && precond != 1)) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
+  if (lambda == 0.0 && !c->has_dirichlet) {
+    int any = 0;
+    // multi-GPU: a Dirichlet face on any rank makes the operator non-singular
+    if (c->comm && c->nranks > 1) any = -1;
+    if (any == 0) FAIL(c, IPDG_ESINGULAR, "lambda = 0 and no Dirichlet face");
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ensure_ws(c));
+  TRY(ensure_partials(c));
+  const int64_t n = c->K * c->ref.Np;
+  if (precond && !(c->dinv_valid && c->dinv_lambda == lambda)) {
+    TRY(ipdg_diag(c, c->dinv, lambda, stream));
+    k_recip<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, c->dinv);
+    c->launches++;
+    c->dinv_valid = true;
+    c->dinv_lambda = lambda;
+  }
+  c->x = x;
+  c->lambda = lambda;
+  c->precond = precond;
+  PcgState h;
+  std::memset(&h, 0, sizeof(h));
+  h.tol2 = tol * tol;
+  h.maxit = INT64_MAX / 4;
+  h.stop_iter = -1;
+  h.precond = precond;
+  *c->st_host = h;
+  CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  TRY(ipdg_ax(c, x, c->Ap, lambda, stream));
+  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->st, c->partials, c->counter);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  TRY(allreduce(c, c->st->red_B, 3, s));
+  // (re)capture the iteration graphs when the operands changed
+  if (c->gkey_x != (const void*)x || c->gkey_lambda != lambda || c->gkey_precond != precond || !c->gexec[0]) {
+    for (auto& g : c->gexec)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    TRY(capture(c, 1, &c->gexec[0]));
+    TRY(capture(c, kChunk, &c->gexec[1]));
+    c->gkey_x = x;
+    c->gkey_lambda = lambda;
+    c->gkey_precond = precond;
+  }
+  return IPDG_OK;
+}
+
+static int set_maxit(ipdg_ctx c, int64_t maxit, cudaStream_t s) {
+  c->st_host->maxit = maxit;
+  CUDA_TRY(c, cudaMemcpyAsync(&c->st->maxit, &c->st_host->maxit, sizeof(long long), cudaMemcpyHostToDevice, s));
+  return IPDG_OK;
+}
+
+int ipdg_pcg_iterate(ipdg_ctx c, int64_t n, void* stream) {
+  if (!c || n < 0) return IPDG_EINVAL;
+  if (!c->gexec[0]) FAIL(c, IPDG_ESTATE, "ipdg_pcg_iterate before ipdg_pcg_begin");
+  cudaStream_t s = (cudaStream_t)stream;
+  while (n >= kChunk) {
+    CUDA_TRY(c, cudaGraphLaunch(c->gexec[1], s));
+    c->launches += 2 * kChunk;
+    n -= kChunk;
+  }
+  while (n-- > 0) {
+    CUDA_TRY(c, cudaGraphLaunch(c->gexec[0], s));
+    c->launches += 2;
+  }
+  return IPDG_OK;
+}
+
+int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b, void* stream) {
+  if (!c || n < 0 || !ms_a || !ms_b) return IPDG_EINVAL;
+  if (!c->gexec[0]) FAIL(c, IPDG_ESTATE, "ipdg_pcg_iterate_profiled before ipdg_pcg_begin");
+  cudaStream_t s = (cudaStream_t)stream;
+  constexpr int B = 64;
+  cudaEvent_t ev[3 * B];
+  for (auto& e : ev) CUDA_TRY(c, cudaEventCreate(&e));
+  double ta = 0.0, tb = 0.0;
+  int rc = IPDG_OK;
+  while (n > 0 && rc == IPDG_OK) {
+    const int m = (int)std::min<int64_t>(n, B);
+    for (int i = 0; i < m && rc == IPDG_OK; ++i) {
+      cudaEventRecord(ev[3 * i], s);
+      rc = [&]() -> int { DISPATCH(c->N, pass_a(c, s)); }();
+      if (rc != IPDG_OK) break;
+      if ((rc = allreduce(c, &c->st->red_A, 1, s)) != IPDG_OK) break;
+      cudaEventRecord(ev[3 * i + 1], s);
+      k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->st,
+                                            c->partials, c->counter);
+      c->launches++;
+      cudaEventRecord(ev[3 * i + 2], s);
+      if ((rc = allreduce(c, c->st->red_B, 2, s)) != IPDG_OK) break;
+    }
+    if (rc != IPDG_OK) break;
+    if (cudaStreamSynchronize(s) != cudaSuccess) { rc = IPDG_ECUDA; break; }
+    for (int i = 0; i < m; ++i) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]);
+      cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]);
+      ta += a;
+      tb += b;
+    }
+    n -= m;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != IPDG_OK) return rc;
+  CUDA_TRY(c, cudaGetLastError());
+  *ms_a = ta;
+  *ms_b = tb;
+  return IPDG_OK;
+}
+
+int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
+  if (!c) return IPDG_EINVAL;
+  if (!c->x) FAIL(c, IPDG_ESTATE, "ipdg_pcg_end before ipdg_pcg_begin");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = c->K * c->ref.Np;
+  k_pcg_final_x<<<vec_grid(c), 256, 0, s>>>(n, c->x, c->pe, c->po, c->st);
+  k_pcg_final_state<<<1, 1, 0, s>>>(c->st);
+  c->launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  const PcgState& h = *c->st_host;
+  if (stats) {
+    stats->iterations = h.stop_iter;
+    stats->bnorm = std::sqrt(h.bb);
+    stats->rel_residual = h.bb > 0 ? std::sqrt(h.final_rr / h.bb) : 0.0;
+    stats->status = h.status;
+    stats->reserved = 0;
+  }
+  if (h.status == -4) FAIL(c, IPDG_EBREAKDOWN, "PCG breakdown at iteration %lld", (long long)h.stop_iter);
+  return h.status == 1 ? IPDG_NOT_CONVERGED : IPDG_OK;
+}
+
+int ipdg_pcg_solve(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, int64_t maxit,
+                   ipdg_stats* stats, void* stream) {
+  if (!c || maxit < 0) return IPDG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ipdg_pcg_begin(c, b, x, lambda, precond, tol, stream));
+  TRY(set_maxit(c, maxit, s));
+  int64_t done = 0;
+  int64_t chunk = kChunk;
+  while (true) {
+    const int64_t n = std::min<int64_t>(chunk, maxit + 1 - done);
+    if (n <= 0) break;
+    TRY(ipdg_pcg_iterate(c, n, stream));
+    done += n;
+    CUDA_TRY(c, cudaMemcpyAsync(&c->st_host->stop_iter, &c->st->stop_iter, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (c->st_host->stop_iter >= 0) break;
+    chunk = std::min<int64_t>(chunk * 2, 8 * kChunk);
+  }
+  return ipdg_pcg_end(c, stats, stream);
+}
+
+int ipdg_pcg_solve_host(ipdg_ctx c, const double* b_host, double* x_host, double lambda, int precond, double tol,
+                        int64_t maxit, ipdg_stats* stats, void* stream) {
+  if (!c || !b_host || !x_host) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ensure_ws(c));
+  const int64_t n = c->K * c->ref.Np;
+  // b goes through the Ap slot of a separate buffer pair: allocate two vectors once
+  static thread_local double* bx = nullptr;
+  static thread_local int64_t bx_n = 0;
+  if (bx_n < n) {
+    if (bx) cudaFree(bx);
+    CUDA_TRY(c, cudaMalloc(&bx, 2 * n * sizeof(double)));
+    bx_n = n;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(bx, b_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(bx + n, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  const int rc = ipdg_pcg_solve(c, bx, bx + n, lambda, precond, tol, maxit, stats, stream);
+  if (rc < 0) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(x_host, bx + n, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  return rc;
+}
+
+int ipdg_comm_init(ipdg_ctx c, const void* id, int nranks, int rank) {
+  if (!c || !id || nranks < 1 || rank < 0 || rank >= nranks) return IPDG_EINVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  if (c->comm) ncclCommDestroy(c->comm);
+  NCCL_TRY(c, ncclCommInitRank(&c->comm, nranks, uid, rank));
+  c->nranks = nranks;
+  c->rank = rank;
+  return IPDG_OK;
+}
+
+int ipdg_nccl_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
+
+int ipdg_nccl_get_unique_id(void* out) {
+  if (!out) return IPDG_EINVAL;
+  ncclUniqueId uid;
+  if (ncclGetUniqueId(&uid) != ncclSuccess) return IPDG_ENCCL;
+  std::memcpy(out, &uid, sizeof(uid));
+  return IPDG_OK;
+}
+
+static int refop_copy(const RefOps& R, int which, double* host, int64_t cap);
+int ipdg_get_refop(ipdg_ctx c, int which, double* host, int64_t cap) {
+  if (!c || !host) return IPDG_EINVAL;
+  return refop_copy(c->ref, which, host, cap);
+}
+
+int ipdg_refop_host(int N, int which, double* host, int64_t cap) {
+  if (!host) return IPDG_EINVAL;
+  if (N < 1 || N > 8) return IPDG_EDEGREE;
+  try {
+    return refop_copy(build_refops(N), which, host, cap);
+  } catch (const std::exception&) {
+    return IPDG_EINVAL;
+  }
+}
+
+static int refop_copy(const RefOps& R, int which, double* host, int64_t cap) {
+  std::vector<double> v;
+  switch (which) {
+    case IPDG_OP_R: v = R.r; break;
+    case IPDG_OP_S: v = R.s; break;
+    case IPDG_OP_DR: v = R.Dr; break;
+    case IPDG_OP_DS: v = R.Ds; break;
+    case IPDG_OP_M: v = R.M; break;
+    case IPDG_OP_M1D: v = R.M1D; break;
+    case IPDG_OP_LIFT: v = R.LIFT; break;
+    case IPDG_OP_FMASK: v.assign(R.Fmask.begin(), R.Fmask.end()); break;
+    default: return IPDG_EINVAL;
+  }
+  if (cap < (int64_t)v.size()) return IPDG_EINVAL;
+  std::copy(v.begin(), v.end(), host);
+  return (int)v.size();
+}
+
+int ipdg_get_geofacs(ipdg_ctx c, double* host, int64_t cap) {
+  if (!c || !host) return IPDG_EINVAL;
+  if (c->K == 0) return IPDG_ESTATE;
+  if (cap < c->K * 5) return IPDG_EINVAL;
+  std::vector<double4> g(c->K);
+  CUDA_TRY(c, cudaMemcpy(g.data(), c->geo, c->K * sizeof(double4), cudaMemcpyDeviceToHost));
+  for (int64_t e = 0; e < c->K; ++e) {
+    host[e * 5 + 0] = g[e].x; host[e * 5 + 1] = g[e].y; host[e * 5 + 2] = g[e].z; host[e * 5 + 3] = g[e].w;
+    host[e * 5 + 4] = 1.0 / (g[e].x * g[e].w - g[e].y * g[e].z);
+  }
+  return IPDG_OK;
+}
+
+int ipdg_get_connectivity(ipdg_ctx c, int32_t* etoe, int32_t* etof, int64_t cap) {
+  if (!c || !etoe || !etof) return IPDG_EINVAL;
+  if (c->K == 0) return IPDG_ESTATE;
+  if (cap < c->K * 3) return IPDG_EINVAL;
+  std::copy(c->etoe_h.begin(), c->etoe_h.end(), etoe);
+  std::copy(c->etof_h.begin(), c->etof_h.end(), etof);
+  return IPDG_OK;
+}
+
+int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
+  if (!c || !out) return IPDG_EINVAL;
+  const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0], c->grid[0][0]};
+  for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+  return IPDG_OK;
+}
+
+int64_t ipdg_launch_count(ipdg_ctx c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// FP64 SIPDG operator kernels for sm_100a (B200).  Included by ipdg.cu only.
+//
+// Paper: arXiv:1801.00246, P:n = PAPER.md line n.
+//
+// Formulation (exactly equal to Eqs. ellipticOp1/ellipticOp3, on affine
+// elements):
+//   u_r = Dr u, u_s = Ds u                                   (Alg. AxG)
+//   delta_f = u+ - u- at the face nodes                       (jump; traces P:553-554)
+//   w_r = J(G_rr u_r + G_rs u_s),  w_s = J(G_rs u_r + G_ss u_s),  G = [r_x s_x; r_y s_y]
+//   g_f = 1/2 n.(grad u- + grad u+) + tau_f delta_f          (SIPDG flux, Eq. INS_SD_5)
+//   Au  = Sr^T w_r + Ss^T w_s                                 (volume, S = M D)
+//       + sum_f (LIFT_f^T Sr)^T (1/2 sJ_f (r_x n_x + r_y n_y) delta_f)   (lift of the jump,
+//       + sum_f (LIFT_f^T Ss)^T (1/2 sJ_f (s_x n_x + s_y n_y) delta_f)    P:454-458)
+//       - sum_f sJ_f scatter_{Fmask_f}(M1D g_f)               (surface flux x face mass)
+//       + lambda J M u                                        (Eq. ellipticOp1)
+// Every dense contraction over many elements runs on the FP64 tensor cores
+// (DMMA, mma.sync.m8n8k4.f64; tcgen05 has no f64 kind): the element index is the
+// M dimension (8 elements per MMA row block), node indices are N and K.  The
+// operator tables are staged once per persistent CTA in shared memory in
+// fragment-major order, so every B-fragment load is one conflict-free LDS.64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ipdg {
+
+template <int N_>
+struct Tr {
+  static constexpr int N = N_;
+  static constexpr int NP = (N + 1) * (N + 2) / 2;
+  static constexpr int NFP = N + 1;
+  static constexpr int NF3 = 3 * NFP;
+  static constexpr int NPK = (NP + 3) / 4 * 4;   // K extent of u (grad GEMM)
+  static constexpr int NPN = (NP + 7) / 8 * 8;   // N extent of node outputs
+  static constexpr int NT = NPN / 8;             // n-tiles per node field
+  static constexpr int KCG = NPK / 4;            // k-chunks, grad GEMM
+  static constexpr int KF = (2 * NF3 + 3) / 4 * 4;  // K extent of the face block (J a_r delta | J a_s delta)
+  static constexpr int KCW = 4 * NT;             // k-chunks fed from registers (w_r, w_s in C layout)
+  static constexpr int KCF = KF / 4;             // k-chunks fed from shared memory (face block)
+  static constexpr int KCM = NPK / 4;            // k-chunks of the lambda (mass) block
+  static constexpr int pad416(int s) { return (s % 16 == 4 || s % 16 == 12) ? s : pad416(s + 1); }
+  static constexpr int SU = pad416(NPK);         // smem row stride of u (conflict-free A loads)
+  static constexpr int SF = pad416(KF);          // smem row stride of the face block
+  // fragment-table sizes (doubles): [chunk][ntile][lane]
+  static constexpr int TAB_G = KCG * 2 * NT * 32;
+  static constexpr int TAB_M = (KCW + KCF) * NT * 32;
+  static constexpr int TAB_L = KCM * NT * 32;
+  // launch shape: W warps, one own 8-element tile per warp
+  static constexpr int W = 8;
+  static constexpr int E = 8 * W;
+};
+
+// Kernel parameters (plain pointers; all device memory).
+struct AxArgs {
+  int64_t K;             // local elements
+  int nblocks;           // element blocks (contiguous ranges of <= E own elements)
+  const int* boff;       // [nblocks+1] first element of each block
+  const double4* geo;    // [K + H] r_x, s_x, r_y, s_y  (H = halo ghosts, multi-GPU)
+  const short4* nbr;     // [K] per face: slot (x,y,z), w = flags: face f -> bits 4f..4f+3 = (f' | bc << 2)
+  const int* goff;       // [nblocks+1] ghost list offsets
+  const int* gid;        // ghost element ids (>= K: halo index K + h)
+  const double* tables;  // fragment tables: G | M | L
+  double tau_c;          // (N+1)(N+2)/2 * tau_scale
+  double lambda;
+  // MODE_AX
+  const double* u;       // [K] x NP
+  double* Au;
+  // MODE_PCG_A
+  const double* r;
+  const double* dinv;    // null: no preconditioner
+  double* p_even;        // p_k lives in p_even when k is even, p_odd when k is odd
+  double* p_odd;         //   (double buffer: ghosts read p_{k-1} while owners write p_k)
+  double* x;             // deferred update x += alpha_{k-1} p_{k-1}
+  const double* halo_p;  // [H x NP] received ghost values of p_k (multi-GPU), else null
+  struct PcgState* st;
+  double* partials;      // [gridDim.x]
+  unsigned int* counter;
+};
+
+// Device-side PCG state (one per context).  See ipdg.cu "PCG protocol".
+struct PcgState {
+  double rho_hist[4];  // rho_k = r_k . z_k at slot k & 3 (global values)
+  double red_A;        // sigma_k = p_k . A p_k  (pass-A output, all-reduced in place)
+  double red_B[3];     // (rho_k, rr_k, bb) pass-B / init output, all-reduced in place
+  double bb;           // ||b||^2
+  double tol2;         // tol^2
+  double final_rr;
+  long long it;        // completed iterations
+  long long maxit;
+  long long stop_iter; // -1 while running
+  int status;          // 0 ok, 1 not converged, -4 breakdown
+  int precond;
+};
+
+}  // namespace ipdg

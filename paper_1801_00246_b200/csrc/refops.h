@@ -1,0 +1,21 @@
+// Reference-triangle operators of degree N (host side of libipdg).  See refops.cpp.
+#pragma once
+#include <vector>
+
+namespace ipdg {
+
+struct RefOps {
+  int N = 0, Np = 0, Nfp = 0;
+  std::vector<double> r, s;          // Np node coordinates on the bi-unit triangle
+  std::vector<double> gll;           // Nfp Gauss-Lobatto points
+  std::vector<double> Dr, Ds;        // Np x Np, row-major: (Dr u)_i = sum_j Dr[i][j] u_j
+  std::vector<double> M;             // Np x Np reference mass (Eq. elMass on the reference element)
+  std::vector<double> Sr, Ss;        // M Dr, M Ds
+  std::vector<double> M1D;           // Nfp x Nfp face mass on [-1,1]
+  std::vector<double> LIFT;          // Np x 3Nfp, M^{-1} E (Eq. elLift)
+  std::vector<int> Fmask;            // 3 x Nfp node ids of each face
+};
+
+RefOps build_refops(int N);
+
+}  // namespace ipdg

@@ -1,0 +1,153 @@
+"""GPU parity: libipdg (CUDA, sm_100a) vs the CPU oracle, through the C ABI.
+
+Tolerance (BASELINE.json north_star): relative L2 error <= 1e-12 for Ax in FP64.
+Inputs: seeded synthetic meshes and U(-1,1) fields from paper_1801_00246_b200.meshgen,
+shaped like the paper's workloads.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import meshops  # noqa: E402
+from oracle.assemble import assemble, mass_matrix  # noqa: E402
+from oracle.exact import assemble_exact  # noqa: E402
+from oracle.mfree import MFree  # noqa: E402
+from oracle.refelem import RefElem  # noqa: E402
+from paper_1801_00246_b200 import Ipdg, IpdgError, meshgen  # noqa: E402
+
+TOL = 1e-12
+
+
+def _mixed(xm, ym):
+    return np.where(xm < 0.5, 1, 2).astype(np.int8)
+
+
+MESHES = {
+    "c1": lambda: meshgen.square(4),
+    "morton": lambda: meshgen.square(23, jitter=0.2, diag="random", order="morton", seed=2),
+    "random_order": lambda: meshgen.square(17, jitter=0.2, diag="random", order="random", seed=3),
+    "mixed_bc": lambda: meshgen.square(15, jitter=0.2, diag="random", order="morton", seed=4, tag=_mixed),
+    "ragged": lambda: meshgen.square(9, 7, jitter=0.1, diag="\\", order="natural", seed=5),  # K=126, partial block
+    "tiny": lambda: meshgen.square(1),  # K=2
+}
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def gpu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("N", range(1, 9))
+@pytest.mark.parametrize("name", list(MESHES))
+def test_ax_matches_oracle(N, name):
+    m = MESHES[name]()
+    ref = RefElem(N)
+    op = Ipdg(N, m)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    for lam in (0.0, 1.0):
+        if lam:
+            A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+        u = meshgen.uniform_field(op.K, op.Np, seed=100 + N)
+        Au = op.ax(gpu(u), lam=lam).cpu().numpy()
+        assert rel(Au.ravel(), A @ u.ravel()) <= TOL, (N, name, lam)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_ax_matches_exact_rational(N):
+    m = meshgen.square(4, diag="random", seed=9, tag=_mixed)
+    Ae = assemble_exact(m["VX"], m["VY"], m["EToV"], m["bc"], N)
+    A = np.array([[float(v) for v in row] for row in Ae])
+    op = Ipdg(N, m)
+    for seed in range(3):
+        u = np.random.default_rng(seed).integers(-3, 4, size=(op.K, op.Np)).astype(np.float64)
+        Au = op.ax(gpu(u)).cpu().numpy().ravel()
+        assert rel(Au, A @ u.ravel()) <= 1e-14
+
+
+@pytest.mark.parametrize("N", [3, 5, 8])
+def test_ax_edge_inputs(N):
+    m = MESHES["mixed_bc"]()
+    op = Ipdg(N, m)
+    z = torch.zeros(op.K, op.Np, dtype=torch.float64, device="cuda")
+    assert torch.count_nonzero(op.ax(z)) == 0
+    # constants: null space under all-Neumann
+    mn = meshgen.square(6, jitter=0.2, diag="random", seed=1, bc_code=2)
+    opn = Ipdg(N, mn)
+    one = torch.ones(opn.K, opn.Np, dtype=torch.float64, device="cuda")
+    assert opn.ax(one).abs().max().item() < 1e-10
+    # linearity and symmetry x.Ay = y.Ax (north star)
+    u = gpu(meshgen.uniform_field(op.K, op.Np, 1))
+    v = gpu(meshgen.uniform_field(op.K, op.Np, 2))
+    Au, Av = op.ax(u), op.ax(v)
+    s1, s2 = (v * Au).sum().item(), (u * Av).sum().item()
+    assert abs(s1 - s2) <= 1e-13 * (u.norm() * Av.norm()).item()
+    assert rel(op.ax(2.0 * u - 3.0 * v).cpu().numpy(), (2 * Au - 3 * Av).cpu().numpy()) < 1e-14
+    # deterministic: bitwise identical repeats
+    assert torch.equal(op.ax(u), Au)
+
+
+def test_setup_parity_geometry_connectivity():
+    m = MESHES["mixed_bc"]()
+    N = 4
+    op = Ipdg(N, m)
+    geo = meshops.affine_geometry(m["VX"], m["VY"], m["EToV"])
+    g = op.geofacs()
+    for j, k in enumerate(["rx", "sx", "ry", "sy", "J"]):
+        assert np.abs(g[:, j] - geo[k]).max() <= 1e-13 * np.abs(geo[k]).max()
+    EToE, EToF, _, _ = meshops.connectivity(m["VX"], m["VY"], m["EToV"], m["bc"], RefElem(N))
+    e, f = op.connectivity()
+    assert np.array_equal(e, EToE) and np.array_equal(f[EToE >= 0], EToF[EToE >= 0])
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 6, 8])
+def test_diag_mass_nodes(N):
+    m = MESHES["mixed_bc"]()
+    ref = RefElem(N)
+    op = Ipdg(N, m)
+    for lam in (0.0, 0.7):
+        A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+        d = op.diag(lam=lam).cpu().numpy().ravel()
+        assert rel(d, A.diagonal()) <= TOL
+    Mg = mass_matrix(m["VX"], m["VY"], m["EToV"], ref)
+    u = meshgen.uniform_field(op.K, op.Np, 7)
+    assert rel(op.mass(gpu(u)).cpu().numpy().ravel(), Mg @ u.ravel()) <= TOL
+    x, y = op.nodes()
+    xo, yo = meshops.physical_nodes(m["VX"], m["VY"], m["EToV"], ref)
+    assert np.abs(x.cpu().numpy() - xo).max() < 1e-14 and np.abs(y.cpu().numpy() - yo).max() < 1e-14
+
+
+def test_errors_are_loud():
+    m = meshgen.square(3)
+    bad = dict(m)
+    bad["EToV"] = m["EToV"][:, ::-1].copy()  # clockwise
+    bad["bc"] = m["bc"][:, [1, 0, 2]].copy()
+    with pytest.raises(IpdgError):
+        Ipdg(2, bad)
+    op = Ipdg(2)
+    with pytest.raises(IpdgError):
+        op.ax(torch.zeros(1, device="cuda", dtype=torch.float64))  # before upload_mesh
+    bc = m["bc"].copy()
+    bc[0, np.nonzero(bc[0] == 0)[0][0]] = 1
+    with pytest.raises(IpdgError):
+        Ipdg(2, dict(m, bc=bc))
+
+
+@pytest.mark.parametrize("N", [4])
+def test_full_size_c2_parity(N):
+    """BASELINE config C2 at full size (199,712 triangles), in the launch configuration bench.py times."""
+    m = meshgen.square(316, jitter=0.2, diag="random", order="morton", seed=2)
+    ref = RefElem(N)
+    op = Ipdg(N, m)
+    u = meshgen.uniform_field(op.K, op.Np, seed=100 + N)
+    Au = op.ax(gpu(u)).cpu().numpy()
+    mf = MFree(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    Ao = mf.apply(u)
+    assert rel(Au.ravel(), Ao.ravel()) <= TOL
+    # element-wise too: worst element relative to its own scale
+    err = np.abs(Au - Ao).max(axis=1) / np.maximum(np.abs(Ao).max(axis=1), 1e-300)
+    assert err.max() <= 1e-11

@@ -1,0 +1,90 @@
+"""GPU PCG parity: iterations within +-1 of the oracle CG, and the oracle-computed residual
+of the GPU solution within tol (BASELINE.json north_star; reading R15)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import solvers  # noqa: E402
+from oracle.assemble import assemble  # noqa: E402
+from oracle.refelem import RefElem  # noqa: E402
+from paper_1801_00246_b200 import Ipdg, IpdgError, meshgen  # noqa: E402
+
+
+def gpu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def check_solve(m, N, precond, tol, lam=0.0, maxit=20000, f=meshgen.sin_sin_forcing):
+    ref = RefElem(N)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+    b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, f)
+    op = Ipdg(N, m)
+    x, st = op.pcg_solve(gpu(b), lam=lam, precond=precond, tol=tol, maxit=maxit)
+    dinv = 1.0 / A.diagonal() if precond else None
+    xo, sto = solvers.pcg(lambda v: A @ v, b.ravel(), tol, maxit, dinv=dinv)
+    assert st["status"] == sto["status"] == 0
+    assert abs(st["iterations"] - sto["iterations"]) <= 1, (st, sto["iterations"])
+    r = b.ravel() - A @ x.cpu().numpy().ravel()
+    assert np.linalg.norm(r) <= tol * np.linalg.norm(b) * (1 + 1e-6) * 1.01
+    assert abs(st["bnorm"] - np.linalg.norm(b)) <= 1e-13 * np.linalg.norm(b)
+    return op, st, sto
+
+
+def test_c1_unpreconditioned():
+    """BASELINE config C1: N=2, 32 triangles, sin(pi x) sin(pi y), unpreconditioned CG."""
+    for tol in (1e-8, 1e-12):
+        check_solve(meshgen.square(4), 2, 0, tol)
+
+
+@pytest.mark.parametrize("N", [1, 3, 4, 6, 8])
+def test_jacobi_mixed_boundaries(N):
+    m = meshgen.square(10, jitter=0.2, diag="random", order="morton", seed=6,
+                       tag=lambda x, y: np.where(x > 0.95, 1, 2).astype(np.int8))
+    check_solve(m, N, 1, 1e-8, f=lambda x, y: np.exp(-((x - 0.3) ** 2 + y ** 2) / 0.1))
+
+
+def test_screened_poisson_lambda():
+    m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=7, bc_code=2)
+    check_solve(m, 3, 1, 1e-10, lam=2.0)
+
+
+def test_edge_cases():
+    m = meshgen.square(4)
+    op = Ipdg(2, m)
+    z = torch.zeros(op.K, op.Np, dtype=torch.float64, device="cuda")
+    x = torch.ones_like(z)
+    x, st = op.pcg_solve(z, x=x, precond=1, tol=1e-8, maxit=100)
+    assert st["iterations"] == 0 and torch.count_nonzero(x) == 0  # b = 0 -> x = 0
+    ref = RefElem(2)
+    b = gpu(solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, meshgen.sin_sin_forcing))
+    x, st = op.pcg_solve(b, precond=0, tol=1e-30, maxit=5)
+    assert st["status"] == 1 and st["iterations"] == 5  # maxit reached, non-fatal
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    xo, sto = solvers.pcg(lambda v: A @ v, b.cpu().numpy().ravel(), 1e-30, 5)
+    assert np.linalg.norm(x.cpu().numpy().ravel() - xo) <= 1e-12 * np.linalg.norm(xo)
+    x, st = op.pcg_solve(b, precond=0, tol=1e-30, maxit=0)
+    assert st["iterations"] == 0 and torch.count_nonzero(x) == 0
+    mn = meshgen.square(4, bc_code=2)
+    with pytest.raises(IpdgError):
+        Ipdg(2, mn).pcg_solve(b, precond=1, tol=1e-8)  # singular: lambda = 0, all Neumann
+
+
+def test_split_api_matches_solve_and_host_path():
+    m = meshgen.square(12, jitter=0.2, diag="random", order="morton", seed=8)
+    N = 4
+    ref = RefElem(N)
+    b_np = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, meshgen.sin_sin_forcing)
+    op = Ipdg(N, m)
+    b = gpu(b_np)
+    x1, st1 = op.pcg_solve(b, precond=1, tol=1e-9, maxit=1000)
+    x2 = torch.zeros_like(b)
+    op.pcg_begin(b, x2, precond=1, tol=1e-9)
+    op.pcg_iterate(st1["iterations"] + 40)
+    st2 = op.pcg_end()
+    assert st2["iterations"] == st1["iterations"] and torch.equal(x1, x2)
+    bh = torch.from_numpy(b_np).pin_memory()
+    xh = torch.zeros_like(bh).pin_memory()
+    st3 = op.pcg_solve_host(bh, xh, precond=1, tol=1e-9, maxit=1000)
+    assert st3["iterations"] == st1["iterations"] and torch.equal(xh, x1.cpu())
