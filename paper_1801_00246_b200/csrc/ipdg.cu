@@ -55,7 +55,7 @@ struct ipdg_ctx_s {
   double* diagtab = nullptr;
   int nblocks = 0, gmax = 0;
   int E = 0;
-  size_t smem[2] = {0, 0};
+  size_t smem[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
   int grid[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
   // host copies for introspection
   std::vector<int> etoe_h, etof_h;
@@ -151,8 +151,16 @@ struct Impl {
             v = at(c < 2 * NT ? R.Sr : R.Ss, NP, i, n, NP, NP);
           } else {
             const int m = 4 * (c - 4 * NT) + (l & 3);
-            if (m < NF3) v = at(LSr, NP, m, n, NF3, NP);
-            else if (m < 2 * NF3) v = at(LSs, NP, m - NF3, n, NF3, NP);
+            const int blk = m / T::NF3P, mm = m % T::NF3P;  // three face sub-blocks, each padded to NF3P
+            if (mm >= NF3) v = 0.0;
+            else if (blk == 0) v = at(LSr, NP, mm, n, NF3, NP);
+            else if (blk == 1) v = at(LSs, NP, mm, n, NF3, NP);
+            else {  // face mass scattered to the face rows: E[n][m'] (E = M LIFT)
+              const int f = mm / NFP, kk = mm % NFP;
+              if (n < NP)
+                for (int q = 0; q < NFP; ++q)
+                  if (R.Fmask[f * NFP + q] == n) v = R.M1D[q * NFP + kk];
+            }
           }
           tm[(c * NT + j) * 32 + l] = v;
         }
@@ -215,18 +223,18 @@ struct Impl {
   }
 
   static int configure(ipdg_ctx c) {
+    int optin = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
     for (int lam = 0; lam < 2; ++lam) {
-      const SmemLayout L = SmemLayout::make<N>(c->gmax, lam != 0);
-      const size_t bytes = (size_t)L.total * sizeof(double);
-      c->smem[lam] = bytes;
       for (int mode = 0; mode < 2; ++mode) {
+        const SmemLayout L = SmemLayout::make<N>(c->gmax, lam != 0, mode == 1);
+        const size_t bytes = (size_t)L.total * sizeof(double);
+        c->smem[mode][lam] = bytes;
         const void* fn = (mode == 0) ? (lam ? (const void*)k_sipdg<N, MODE_AX, true> : (const void*)k_sipdg<N, MODE_AX, false>)
                                      : (lam ? (const void*)k_sipdg<N, MODE_PCG_A, true>
                                             : (const void*)k_sipdg<N, MODE_PCG_A, false>);
         // opt in to the full per-CTA maximum once: the attribute is per function (shared by all
         // contexts of this N), the launch passes the context's own byte count
-        int optin = 0;
-        CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
         if ((int)bytes > optin - 1024) FAIL(c, IPDG_ECUDA, "k_sipdg<N=%d> needs %zu B of shared memory", N, bytes);
         CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         int occ = 0;
@@ -260,8 +268,8 @@ struct Impl {
     a.lambda = lambda;
     const bool lam = lambda != 0.0;
     const int g = c->grid[0][lam];
-    if (lam) k_sipdg<N, MODE_AX, true><<<g, T::W * 32, c->smem[1], s>>>(a, c->gmax);
-    else k_sipdg<N, MODE_AX, false><<<g, T::W * 32, c->smem[0], s>>>(a, c->gmax);
+    if (lam) k_sipdg<N, MODE_AX, true><<<g, T::W * 32, c->smem[0][1], s>>>(a, c->gmax);
+    else k_sipdg<N, MODE_AX, false><<<g, T::W * 32, c->smem[0][0], s>>>(a, c->gmax);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return IPDG_OK;
@@ -281,8 +289,8 @@ struct Impl {
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
     const int g = c->grid[1][lam];
-    if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1], s>>>(a, c->gmax);
-    else k_sipdg<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem[0], s>>>(a, c->gmax);
+    if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1][1], s>>>(a, c->gmax);
+    else k_sipdg<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem[1][0], s>>>(a, c->gmax);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return IPDG_OK;
@@ -349,8 +357,8 @@ static int ghost_cap_n(int device) {
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (optin <= 0) optin = 227 * 1024;
-  const int fixed = SmemLayout::make<N>(0, true).total * 8 + 1024;  // + static smem
-  const int per = (T::SU + T::NF3 + 5) * 8;
+  const int fixed = SmemLayout::make<N>(0, true, true).total * 8 + 1024;  // + static smem
+  const int per = (T::SU + T::SG + 2 + std::max(T::SXY, 3 * T::NP)) * 8;
   int g = (optin - fixed) / per;
   g = g / 8 * 8;
   return std::max(8, std::min(g, 30000 - T::E));
@@ -447,6 +455,16 @@ int ipdg_create(ipdg_ctx* out, int N, int device) {
     return IPDG_ECUDA;
   }
   const RefOps& R = c->ref;
+  // the kernels use the closed-form face-node indices of kernels.cuh (fmask_cf); check them
+  for (int f = 0; f < 3; ++f)
+    for (int k = 0; k <= N; ++k) {
+      const int off = k * (N + 1) - k * (k - 1) / 2;
+      const int cf = f == 0 ? k : (f == 1 ? off + N - k : off);
+      if (R.Fmask[f * (N + 1) + k] != cf) {
+        delete c;
+        return IPDG_EDEGREE;
+      }
+    }
   int rc = IPDG_OK;
   std::vector<double> tab = tables_of(R), dtab = diagtab_of(R), rs(2 * R.Np);
   for (int i = 0; i < R.Np; ++i) { rs[i] = R.r[i]; rs[R.Np + i] = R.s[i]; }
@@ -994,7 +1012,7 @@ int ipdg_get_connectivity(ipdg_ctx c, int32_t* etoe, int32_t* etof, int64_t cap)
 
 int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   if (!c || !out) return IPDG_EINVAL;
-  const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0], c->grid[0][0]};
+  const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0]};
   for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
   return IPDG_OK;
 }

@@ -34,21 +34,38 @@ struct Tr {
   static constexpr int NPN = (NP + 7) / 8 * 8;   // N extent of node outputs
   static constexpr int NT = NPN / 8;             // n-tiles per node field
   static constexpr int KCG = NPK / 4;            // k-chunks, grad GEMM
-  static constexpr int KF = (2 * NF3 + 3) / 4 * 4;  // K extent of the face block (J a_r delta | J a_s delta)
+  static constexpr int NF3P = (NF3 + 3) / 4 * 4;   // face nodes padded to whole k-chunks
+  static constexpr int NQ = NF3P / 4;               // face-node passes of the 4 lanes of an element
+  static constexpr int KF = 3 * NF3P;               // K extent of the face block (a_r delta | a_s delta | -sJ g)
   static constexpr int KCW = 4 * NT;             // k-chunks fed from registers (w_r, w_s in C layout)
-  static constexpr int KCF = KF / 4;             // k-chunks fed from shared memory (face block)
+  static constexpr int KCF = KF / 4;             // k-chunks of the face block (fed from registers)
   static constexpr int KCM = NPK / 4;            // k-chunks of the lambda (mass) block
   static constexpr int pad416(int s) { return (s % 16 == 4 || s % 16 == 12) ? s : pad416(s + 1); }
   static constexpr int SU = pad416(NPK);         // smem row stride of u (conflict-free A loads)
   static constexpr int SF = pad416(KF);          // smem row stride of the face block
+  static constexpr int SXY = 2 * NPN + 2;        // smem row stride of (u_x | u_y) per slot (= 2 mod 16: gathers spread over banks)
+  static constexpr int SG = 8;                   // per-slot geometry: rx sx ry sy J det - -
+  static constexpr int RPW = NP >= 32 ? 1 : 32 / NP;  // element rows copied per warp pass
+  static constexpr int NPASS = (NP + 31) / 32;        // lane passes per row (NP > 32)
   // fragment-table sizes (doubles): [chunk][ntile][lane]
   static constexpr int TAB_G = KCG * 2 * NT * 32;
   static constexpr int TAB_M = (KCW + KCF) * NT * 32;
   static constexpr int TAB_L = KCM * NT * 32;
   // launch shape: W warps, one own 8-element tile per warp
-  static constexpr int W = 8;
+  static constexpr int W = N >= 7 ? 4 : 8;
   static constexpr int E = 8 * W;
+  static constexpr int MINB = N <= 5 ? 2 : 1;
+  static constexpr int FGS = E + 8;              // field stride of the per-face geometry (bank spread, see P2)  // CTAs per SM the register allocation must allow
 };
+
+// Face-node index in closed form for the row-by-row node order (refops.cpp; verified at setup):
+// row j (s index) holds N+1-j nodes starting at off(j) = j(N+1) - j(j-1)/2.
+//   face 0 (s = -1):   node k            face 1 (r+s = 0): node off(k) + N - k
+//   face 2 (r = -1):   node off(k)
+template <int N>
+__host__ __device__ __forceinline__ constexpr int fmask_cf(int f, int k) {
+  return f == 0 ? k : (f == 1 ? k * (N + 1) - (k * (k - 1)) / 2 + N - k : k * (N + 1) - (k * (k - 1)) / 2);
+}
 
 // Kernel parameters (plain pointers; all device memory).
 struct AxArgs {

@@ -1,19 +1,19 @@
 // FP64 SIPDG operator, Jacobi diagonal and PCG vector kernels for sm_100a.
 // Paper: arXiv:1801.00246 (P:n = PAPER.md line n).  Formulation in kernels.cuh.
 //
-// Kernel k_sipdg<N, MODE, LAM> (one persistent CTA per SM slot, W warps):
-//   per element block of E = 8W own elements plus the block's G ghost elements
+// Kernel k_sipdg<N, MODE, LAM> (persistent CTAs, W warps, loop over element blocks):
+//   per element block of <= E = 8W own elements plus the block's G ghost elements
 //   (face neighbours outside the block, listed at setup):
-//   P0  load u (or, in PCG pass A, form p = D^{-1} r + beta p_old on the fly) for own
-//       and ghost elements, geometric factors, neighbour slots              -> smem
-//   P1  per 8-element tile: [u_r | u_s] = u [Dr^T | Ds^T] on DMMA; own tiles keep
-//       w_r, w_s = J G (u_r, u_s) in registers (C fragment layout); every tile writes
-//       its face-node normal derivatives n.grad u to smem                   (Alg. AxG)
-//   P2  per own face node: jump delta = u+ - u- (mirrored on boundary faces), flux
-//       g = 1/2 n.(grad u- + grad u+) + tau delta, lift coefficients   (Alg. AxKernel)
-//   P3  per own tile: Au = -sum_f sJ_f scatter(M1D g_f) (accumulator init)
-//       + [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss] on DMMA (+ lambda J u M),
-//       stored element-major; PCG pass A also accumulates p . Ap.
+//   P0  u of own + ghost elements -> smem (Ax: cp.async; PCG pass A: p = D^-1 r + beta p_{k-1}
+//       formed from batched loads, p_k and the deferred x update written back);
+//       per-slot face geometry (J, det G, unit normals, sJ) computed once per slot
+//   P1  per 8-element tile: [u_r | u_s] = u [Dr^T | Ds^T] on DMMA      (Alg. AxG);
+//       u_x, u_y -> smem; own tiles keep w_r, w_s = J G (u_r, u_s) in registers (C layout)
+//   P2  per own face node: delta = u+ - u- (mirrored on boundary faces), flux
+//       g = 1/2 n-.(grad u- + grad u+) + tau delta                     (Alg. AxKernel)
+//       -> face block [1/2 sJ (n.grad r) delta | 1/2 sJ (n.grad s) delta | -sJ g]
+//   P3  per own tile: Au = [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss; E^T] on DMMA
+//       (+ lambda J u M), stored element-major; PCG pass A also accumulates p . Ap.
 #include "kernels.cuh"
 
 namespace ipdg {
@@ -23,15 +23,29 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 enum { MODE_AX = 0, MODE_PCG_A = 1 };
 
 // shared-memory layout (in doubles) shared by host and device
 struct SmemLayout {
-  int tabG, tabM, tabL, m1d, iaux, us, dnt, geo, fa, gs, nb, total;  // offsets in doubles
-  __host__ __device__ static int r2(int x) { return (x + 1) & ~1; }
+  int tabG, tabM, tabL, iaux, us, geo, fg, nb, gid, uxy, fa, stg, total;  // offsets in doubles
   template <int N>
-  __host__ __device__ static SmemLayout make(int gmax, bool lam) {
+  __host__ __device__ static SmemLayout make(int gmax, bool lam, bool pcg) {
     using T = Tr<N>;
     SmemLayout L;
     const int gm8 = (gmax + 7) / 8 * 8;
@@ -40,18 +54,43 @@ struct SmemLayout {
     L.tabG = o; o += T::TAB_G;
     L.tabM = o; o += T::TAB_M;
     L.tabL = o; o += lam ? T::TAB_L : 0;
-    L.m1d = o; o += T::NFP * T::NFP;
-    L.iaux = o; o += r2(T::NF3 + 2 * T::NPN) / 2;  // ints: fmask[NF3], nodeface[2*NPN]
+    L.iaux = o; o += (6 * T::NFP + 1) / 2;  // ints: neighbour face-node index nidx[f'][flip][k]
+    o = (o + 1) & ~1;                   // 16-byte alignment
     L.us = o; o += slots * T::SU;
-    L.dnt = o; o += slots * T::NF3;
-    L.geo = o; o += slots * 5;
-    L.fa = o; o += T::E * T::SF;
-    L.gs = o; o += T::E * T::NF3;
-    L.nb = o; o += T::E;  // short4 per element = 8 bytes
+    o = (o + 1) & ~1;
+    L.geo = o; o += slots * T::SG;
+    L.fg = o; o += 15 * T::FGS;        // own elements: per face n_x n_y sJ c_r c_s, layout [5f + field][e]
+    L.nb = o; o += 2 * T::E;            // short4 per element, double-buffered
+    L.gid = o; o += gm8;                // 2 x gm8 ints, double-buffered
+    o = (o + 1) & ~1;
+    L.uxy = o; o += slots * T::SXY;
+    L.fa = o;  // (face block lives in registers)
+    // PCG staging of r, D^-1, p_{k-1}, x (own) and r, D^-1, p_{k-1} (ghosts) aliases uxy / fa,
+    // which are produced only after the staging has been consumed
+    L.stg = L.uxy;
+    const int need = pcg ? (4 * T::E + 3 * gm8) * T::NP : 0;
+    if (L.stg + need > o) o = L.stg + need;
     L.total = o;
     return L;
   }
 };
+
+// copy loop over element rows: warp-strided rows, lanes across the Np entries of a row
+template <int N, class F>
+__device__ __forceinline__ void for_rows(int nrows, int warp, int lane, F&& f) {
+  using T = Tr<N>;
+  constexpr int NP = T::NP, RPW = T::RPW, W = T::W;
+  const int rsub = (NP >= 32) ? 0 : lane / NP;
+  const int i0 = (NP >= 32) ? lane : lane - rsub * NP;
+  if (rsub >= RPW) return;
+  for (int row = warp * RPW + rsub; row < nrows; row += W * RPW) {
+#pragma unroll
+    for (int ps = 0; ps < T::NPASS; ++ps) {
+      const int i = i0 + 32 * ps;
+      if (i < NP) f(row, i);
+    }
+  }
+}
 
 // deterministic block reduction of NV doubles; result valid in thread 0
 template <int NV>
@@ -92,7 +131,6 @@ __device__ bool grid_reduce(double (&v)[NV], double* red, double* partials, unsi
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
-  // last CTA: fixed-order sum over partials (strided per thread, then block tree)
   double w[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
@@ -110,26 +148,28 @@ __device__ bool grid_reduce(double (&v)[NV], double* red, double* partials, unsi
 }
 
 template <int N, int MODE, bool LAM>
-__global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) {
+__global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, int gmax) {
   using T = Tr<N>;
-  constexpr int NP = T::NP, NFP = T::NFP, NF3 = T::NF3, NT = T::NT, SU = T::SU, SF = T::SF;
+  constexpr int NP = T::NP, NFP = T::NFP, NF3 = T::NF3, NT = T::NT, NPN = T::NPN, SU = T::SU, SF = T::SF;
+  constexpr int SXY = T::SXY, SG = T::SG;
   constexpr int W = T::W, E = T::E, KCG = T::KCG, KCW = T::KCW, KCF = T::KCF, KCM = T::KCM;
+  constexpr int NTHR = W * 32;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32 * 3];
-  const SmemLayout L = SmemLayout::make<N>(gmax, LAM);
+  const SmemLayout L = SmemLayout::make<N>(gmax, LAM, MODE == MODE_PCG_A);
+  const int gm8 = (gmax + 7) / 8 * 8;
   double* tabG = sm + L.tabG;
   double* tabM = sm + L.tabM;
   double* tabL = sm + L.tabL;
-  double* m1d = sm + L.m1d;
-  int* fmask = reinterpret_cast<int*>(sm + L.iaux);
-  int* nodeface = fmask + NF3;
+  int* nidx = reinterpret_cast<int*>(sm + L.iaux);
   double* us = sm + L.us;
-  double* dnt = sm + L.dnt;
   double* geos = sm + L.geo;
-  double* fa = sm + L.fa;
-  double* gs = sm + L.gs;
-  short4* nbs = reinterpret_cast<short4*>(sm + L.nb);
-  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* fgs = sm + L.fg;
+  short4* nbs0 = reinterpret_cast<short4*>(sm + L.nb);
+  int* gids0 = reinterpret_cast<int*>(sm + L.gid);
+  double* uxy = sm + L.uxy;
+  double* stg = sm + L.stg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t K = a.K;
 
   // ---- PCG pass-A prologue: decisions from the previous iteration's reductions
@@ -163,7 +203,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
     }
     if (stop) {
       const int64_t n = K * NP;
-      for (int64_t i = blockIdx.x * (int64_t)nthr + tid; i < n; i += (int64_t)gridDim.x * nthr) {
+      for (int64_t i = blockIdx.x * (int64_t)NTHR + tid; i < n; i += (int64_t)gridDim.x * NTHR) {
         if (zero_x) a.x[i] = 0.0;
         else if (do_xupd) a.x[i] += alpha_prev * pold[i];
       }
@@ -178,75 +218,139 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
     }
   }
 
-  // ---- stage the operator tables and small index tables once per CTA
+  // ---- once per CTA: operator tables, index table, zero padding; neighbour data of block 0
   {
     const double* src = a.tables;
-    const int ntab = T::TAB_G + T::TAB_M + (LAM ? T::TAB_L : 0);
-    for (int i = tid; i < ntab; i += nthr) sm[i] = src[i];
-    const double* aux = a.tables + T::TAB_G + T::TAB_M + T::TAB_L;
-    for (int i = tid; i < NFP * NFP; i += nthr) m1d[i] = aux[i];
-    const int* iaux = reinterpret_cast<const int*>(aux + NFP * NFP);
-    for (int i = tid; i < NF3 + 2 * T::NPN; i += nthr) fmask[i] = iaux[i];
-    // zero the padding columns once: u[NP..SU), face block [2*NF3..SF)
-    const int slots = E + (gmax + 7) / 8 * 8;
-    for (int i = tid; i < slots * SU; i += nthr) us[i] = 0.0;
-    for (int i = tid; i < E * SF; i += nthr) fa[i] = 0.0;
+    constexpr int ntab = T::TAB_G + T::TAB_M + (LAM ? T::TAB_L : 0);  // multiple of 32 doubles
+    for (int i = 2 * tid; i < ntab; i += 2 * NTHR) cp_async16(sm + i, src + i);
+    for (int q = tid; q < 6 * NFP; q += NTHR) {  // nidx[fp][flip][k] = Fmask[fp][flip ? Nfp-1-k : k]
+      const int fp = q / (2 * NFP), fl = (q / NFP) & 1, kk = q % NFP;
+      nidx[q] = fmask_cf<N>(fp, fl ? NFP - 1 - kk : kk);
+    }
+    const int slots = E + gm8;
+    for (int i = tid; i < slots * SU; i += NTHR) us[i] = 0.0;
+    const int b = blockIdx.x;
+    if (b < a.nblocks) {
+      const int e0 = a.boff[b], Eb = a.boff[b + 1] - e0, g0 = a.goff[b], Gb = a.goff[b + 1] - g0;
+      for (int e = tid; e < Eb; e += NTHR) cp_async8(nbs0 + e, a.nbr + e0 + e);
+      for (int g = tid; g < Gb; g += NTHR) gids0[g] = a.gid[g0 + g];
+    }
   }
 
+  // face-node items of this lane (4 lanes per element): fk = 4q + (lane & 3) -> (f, k, node)
+  int itab[T::NQ];
+#pragma unroll
+  for (int q = 0; q < T::NQ; ++q) {
+    const int fk = 4 * q + (lane & 3);
+    const int f = fk / NFP, kk = fk - f * NFP;
+    itab[q] = (fk < NF3) ? ((f << 24) | (kk << 16) | fmask_cf<N>(f, kk)) : -1;
+  }
   double wr[NT][2], ws[NT][2];
-  for (int b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
-    const int64_t e0 = a.boff[b];
-    const int Eb = a.boff[b + 1] - a.boff[b];
-    const int gbeg = a.goff[b];
-    const int Gb = a.goff[b + 1] - gbeg;
-    __syncthreads();
-    // ---- P0: element data into shared memory
-    for (int idx = tid; idx < Eb * NP; idx += nthr) {
-      const int e = idx / NP, i = idx - e * NP;
-      const int64_t g = e0 * NP + idx;
-      double v;
-      if (MODE == MODE_AX) {
-        v = __ldg(a.u + g);
-      } else {
-        const double rr = __ldg(a.r + g);
-        const double z = a.dinv ? rr * __ldg(a.dinv + g) : rr;
-        const double po = first ? 0.0 : pold[g];
-        v = first ? z : z + beta * po;
-        pnew[g] = v;
-        if (do_xupd) a.x[g] += alpha_prev * po;
-      }
-      us[e * SU + i] = v;
-    }
-    for (int idx = tid; idx < Gb * NP; idx += nthr) {
-      const int gq = idx / NP, i = idx - gq * NP;
-      const int ge = a.gid[gbeg + gq];
-      double v;
-      if (ge >= K) {
-        v = a.halo_p[(int64_t)(ge - K) * NP + i];
-      } else {
-        const int64_t g = (int64_t)ge * NP + i;
-        if (MODE == MODE_AX) {
-          v = __ldg(a.u + g);
-        } else {
-          const double rr = __ldg(a.r + g);
-          const double z = a.dinv ? rr * __ldg(a.dinv + g) : rr;
-          v = first ? z : z + beta * pold[g];  // p_{k-1} of a ghost (owner writes p_k elsewhere)
-        }
-      }
-      us[(E + gq) * SU + i] = v;
-    }
-    for (int s = tid; s < Eb + Gb; s += nthr) {
+  int par = 0;
+  int cur_e0 = 0, cur_Eb = 0, cur_Gb = 0;  // block metadata, prefetched one block ahead
+  if (blockIdx.x < a.nblocks) {
+    cur_e0 = a.boff[blockIdx.x];
+    cur_Eb = a.boff[blockIdx.x + 1] - cur_e0;
+    cur_Gb = a.goff[blockIdx.x + 1] - a.goff[blockIdx.x];
+  }
+  for (int b = blockIdx.x; b < a.nblocks; b += gridDim.x, par ^= 1) {
+    const int64_t e0 = cur_e0;
+    const int Eb = cur_Eb;
+    const int Gb = cur_Gb;
+    short4* nbs = nbs0 + par * E;
+    int* gids = gids0 + par * gm8;
+    cp_async_wait_all();
+    __syncthreads();  // previous block done with the buffers; this block's gids / nbr landed
+    // ---- P0: async copies of the element data of this block
+    for (int q = tid; q < 2 * (Eb + Gb); q += NTHR) {  // raw geometry r_x s_x r_y s_y (2 x 16 B)
+      const int s = q >> 1, h = q & 1;
       const int slot = s < Eb ? s : E + (s - Eb);
-      const int64_t el = s < Eb ? e0 + s : (int64_t)a.gid[gbeg + s - Eb];
-      const double4 gg = a.geo[el];
-      double* gp = geos + slot * 5;
-      gp[0] = gg.x; gp[1] = gg.y; gp[2] = gg.z; gp[3] = gg.w;
-      gp[4] = 1.0 / (gg.x * gg.w - gg.y * gg.z);  // J = 1 / det(G)
+      const int64_t el = s < Eb ? e0 + s : (int64_t)gids[s - Eb];
+      cp_async16(geos + slot * SG + 2 * h, reinterpret_cast<const double*>(a.geo + el) + 2 * h);
     }
-    for (int e = tid; e < Eb; e += nthr) nbs[e] = a.nbr[e0 + e];
+    if (MODE == MODE_AX) {
+      const double* u = a.u;
+      for_rows<N>(Eb, warp, lane, [&](int e, int i) { cp_async8(us + e * SU + i, u + (e0 + e) * NP + i); });
+      for_rows<N>(Gb, warp, lane, [&](int g, int i) {
+        const int ge = gids[g];
+        const double* srcp = ge >= K ? a.halo_p + (int64_t)(ge - K) * NP : u + (int64_t)ge * NP;
+        cp_async8(us + (E + g) * SU + i, srcp + i);
+      });
+    } else {
+      double* sr = stg;                  // own: r | dinv | p_{k-1} | x, then ghosts: r | dinv | p_{k-1}
+      double* sd = stg + E * NP;
+      double* sp = stg + 2 * E * NP;
+      double* sx = stg + 3 * E * NP;
+      double* gr = stg + 4 * E * NP;
+      double* gd = gr + gm8 * NP;
+      double* gp = gd + gm8 * NP;
+      const double* dv = a.dinv;
+      for_rows<N>(Eb, warp, lane, [&](int e, int i) {
+        const int64_t g = (e0 + e) * NP + i;
+        cp_async8(sr + e * NP + i, a.r + g);
+        if (dv) cp_async8(sd + e * NP + i, dv + g);
+        if (!first) cp_async8(sp + e * NP + i, pold + g);
+        if (do_xupd) cp_async8(sx + e * NP + i, a.x + g);
+      });
+      for_rows<N>(Gb, warp, lane, [&](int q, int i) {
+        const int ge = gids[q];
+        if (ge >= K) {
+          cp_async8(gr + q * NP + i, a.halo_p + (int64_t)(ge - K) * NP + i);
+        } else {
+          const int64_t g = (int64_t)ge * NP + i;
+          cp_async8(gr + q * NP + i, a.r + g);
+          if (dv) cp_async8(gd + q * NP + i, dv + g);
+          if (!first) cp_async8(gp + q * NP + i, pold + g);  // p_{k-1}; owners write p_k elsewhere
+        }
+      });
+    }
+    cp_async_commit();
+    // prefetch the neighbour slots / ghost ids of this CTA's next block (small, double-buffered)
+    {
+      const int bn = b + gridDim.x;
+      if (bn < a.nblocks) {
+        const int e0n = a.boff[bn], Ebn = a.boff[bn + 1] - e0n, g0n = a.goff[bn], Gbn = a.goff[bn + 1] - g0n;
+        short4* nbn = nbs0 + (par ^ 1) * E;
+        int* gin = gids0 + (par ^ 1) * gm8;
+        for (int e = tid; e < Ebn; e += NTHR) cp_async8(nbn + e, a.nbr + e0n + e);
+        for (int g = tid; g < Gbn; g += NTHR) cp_async4(gin + g, a.gid + g0n + g);
+        cur_e0 = e0n;
+        cur_Eb = Ebn;
+        cur_Gb = Gbn;
+      }
+      cp_async_commit();
+    }
+    cp_async_wait_group1();  // this block's data complete; the prefetch may still fly
     __syncthreads();
+    if (MODE == MODE_PCG_A) {  // p_k = D^-1 r + beta p_{k-1} (own + ghosts); x += alpha_{k-1} p_{k-1}
+      const double* sr = stg;
+      const double* sd = stg + E * NP;
+      const double* sp = stg + 2 * E * NP;
+      const double* sx = stg + 3 * E * NP;
+      const double* gr = stg + 4 * E * NP;
+      const double* gd = gr + gm8 * NP;
+      const double* gp = gd + gm8 * NP;
+      const bool pre = a.dinv != nullptr;
+      for_rows<N>(Eb, warp, lane, [&](int e, int i) {
+        const int o = e * NP + i;
+        const double po = first ? 0.0 : sp[o];
+        const double v = (pre ? sr[o] * sd[o] : sr[o]) + beta * po;
+        const int64_t g = (e0 + e) * NP + i;
+        pnew[g] = v;
+        if (do_xupd) a.x[g] = sx[o] + alpha_prev * po;
+        us[e * SU + i] = v;
+      });
+      for_rows<N>(Gb, warp, lane, [&](int q, int i) {
+        const int o = q * NP + i;
+        double v;
+        if (gids[q] >= K) v = gr[o];
+        else v = (pre ? gr[o] * gd[o] : gr[o]) + (first ? 0.0 : beta * gp[o]);
+        us[(E + q) * SU + i] = v;
+      });
+      __syncthreads();
+    }
 
-    // ---- P1: reference gradient on DMMA, face normal derivatives, w_r / w_s
+    // ---- P1: reference gradient on DMMA; u_x, u_y to smem; w_r / w_s kept for own tiles
     const int ntiles = W + (Gb + 7) / 8;
     for (int t = warp; t < ntiles; t += W) {
       const bool own = t < W;
@@ -264,106 +368,89 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
 #pragma unroll
         for (int q = 0; q < 2 * NT; ++q) dmma(acc[q][0], acc[q][1], av, bt[q * 32]);
       }
-      const double* gp = geos + srow * 5;
-      const double rx = gp[0], sx = gp[1], ry = gp[2], sy = gp[3], J = gp[4];
-      // outward normals (unnormalised g_f = J^{-1} sJ n_f): -grad s, grad r + grad s, -grad r
-      const double g0x = -sx, g0y = -sy, g1x = rx + sx, g1y = ry + sy, g2x = -rx, g2y = -ry;
-      const double i0 = rsqrt(g0x * g0x + g0y * g0y), i1 = rsqrt(g1x * g1x + g1y * g1y), i2 = rsqrt(g2x * g2x + g2y * g2y);
-      const double Grr = rx * rx + ry * ry, Grs = rx * sx + ry * sy, Gss = sx * sx + sy * sy;
+      double* gq = geos + srow * SG;
+      const double rx = gq[0], sx = gq[1], ry = gq[2], sy = gq[3];
+      const double det = rx * sy - sx * ry;  // = 1/J
+      const double J = 1.0 / det;
+      if ((lane & 3) == 0) { gq[4] = J; gq[5] = det; }
+      if (own && (lane & 3) < 3) {  // one face per lane: unit normal, sJ, lift coefficients
+        const int f = lane & 3;
+        const double gx = (f == 0) ? -sx : (f == 1) ? rx + sx : -rx;  // outward: -grad s, grad r+s, -grad r
+        const double gy = (f == 0) ? -sy : (f == 1) ? ry + sy : -ry;
+        const double len = sqrt(gx * gx + gy * gy);
+        const double il = 1.0 / len;
+        double* fq = fgs + 5 * f * T::FGS + srow;
+        fq[0] = gx * il;
+        fq[T::FGS] = gy * il;
+        fq[2 * T::FGS] = J * len;                        // sJ = edge length / 2 (R6)
+        fq[3 * T::FGS] = 0.5 * J * (rx * gx + ry * gy);  // 1/2 sJ (n . grad r)
+        fq[4 * T::FGS] = 0.5 * J * (sx * gx + sy * gy);  // 1/2 sJ (n . grad s)
+      }
+      const double Grr = J * (rx * rx + ry * ry), Grs = J * (rx * sx + ry * sy), Gss = J * (sx * sx + sy * sy);
+      double* xyrow = uxy + srow * SXY + 2 * (lane & 3);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = 8 * nt + 2 * (lane & 3) + h;
-          const double ur = acc[nt][h], usv = acc[NT + nt][h];
-          if (own) {
-            wr[nt][h] = J * (Grr * ur + Grs * usv);
-            ws[nt][h] = J * (Grs * ur + Gss * usv);
-          }
-          if (i < NP) {
-            const double ux = rx * ur + sx * usv, uy = ry * ur + sy * usv;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int nf = nodeface[2 * i + q];
-              if (nf >= 0) {
-                const int f = nf / NFP;
-                const double dn = (f == 0) ? (g0x * ux + g0y * uy) * i0
-                                 : (f == 1) ? (g1x * ux + g1y * uy) * i1
-                                            : (g2x * ux + g2y * uy) * i2;
-                dnt[srow * NF3 + nf] = dn;
-              }
-            }
-          }
+        const double ur0 = acc[nt][0], ur1 = acc[nt][1], us0 = acc[NT + nt][0], us1 = acc[NT + nt][1];
+        *reinterpret_cast<double2*>(xyrow + 8 * nt) = make_double2(rx * ur0 + sx * us0, rx * ur1 + sx * us1);
+        *reinterpret_cast<double2*>(xyrow + NPN + 8 * nt) = make_double2(ry * ur0 + sy * us0, ry * ur1 + sy * us1);
+        if (own) {
+          wr[nt][0] = Grr * ur0 + Grs * us0;
+          wr[nt][1] = Grr * ur1 + Grs * us1;
+          ws[nt][0] = Grs * ur0 + Gss * us0;
+          ws[nt][1] = Grs * ur1 + Gss * us1;
         }
       }
     }
     __syncthreads();
 
-    // ---- P2: jumps, fluxes and lift coefficients at the own face nodes
-    for (int idx = tid; idx < Eb * NF3; idx += nthr) {
-      const int e = idx / NF3, fk = idx - e * NF3;
-      const int f = fk / NFP, kk = fk - f * NFP;
-      const short4 nb = nbs[e];
-      const int flags = nb.w;
-      const int fl = (flags >> (4 * f)) & 15;
-      const int fp = fl & 3, bc = fl >> 2;
-      const int slot = (f == 0) ? nb.x : (f == 1) ? nb.y : nb.z;
-      const double* gp = geos + e * 5;
-      const double rx = gp[0], sx = gp[1], ry = gp[2], sy = gp[3], J = gp[4];
-      const double gx = (f == 0) ? -sx : (f == 1) ? rx + sx : -rx;
-      const double gy = (f == 0) ? -sy : (f == 1) ? ry + sy : -ry;
-      const double glen = sqrt(gx * gx + gy * gy);
-      const double sJ = J * glen;  // half edge length (R6)
-      const double um = us[e * SU + fmask[fk]];
-      const double dnm = dnt[e * NF3 + fk];
-      double up, dnp, invJp;
-      if (bc == 0) {
-        const bool flip = ((f == 2) == (fp == 2));
-        const int kp = flip ? NFP - 1 - kk : kk;
-        up = us[slot * SU + fmask[fp * NFP + kp]];
-        dnp = -dnt[slot * NF3 + fp * NFP + kp];  // neighbour's outward derivative, re-signed to n-
-        invJp = 1.0 / geos[slot * 5 + 4];
-      } else if (bc == 1) {  // Dirichlet mirror
-        up = -um; dnp = dnm; invJp = 0.0;
-      } else {               // Neumann mirror
-        up = um; dnp = -dnm; invJp = 0.0;
-      }
-      const double delta = up - um;  // paper jump
-      const double tau = a.tau_c * sJ * fmax(1.0 / J, invJp);  // Eq. Ch2.PenaltyParameter, 1/h = sJ/J
-      const double gflux = 0.5 * (dnm + dnp) + tau * delta;
-      // 1/2 sJ (r_x n_x + r_y n_y) = 1/2 J (r_x g_x + r_y g_y)
-      fa[e * SF + fk] = 0.5 * J * (rx * gx + ry * gy) * delta;
-      fa[e * SF + NF3 + fk] = 0.5 * J * (sx * gx + sy * gy) * delta;
-      gs[e * NF3 + fk] = -sJ * gflux;
-    }
-    __syncthreads();
-
-    // ---- P3: own tile of this warp -> Au
+    // ---- P2 + P3 per warp on its own tile (no block barrier in between)
     if (8 * warp < Eb) {
+      // P2: four lanes per element, one face node per lane and pass: jumps and fluxes, kept in
+      // registers exactly where the face block's A fragments need them (A[e = lane>>2][k = lane&3])
+      double far[T::NQ], fas[T::NQ], fag[T::NQ];
+      {
+        const int e = 8 * warp + (lane >> 2);
+        const int ec = e < Eb ? e : 8 * warp;  // rows past the block end compute on a valid slot, never stored
+        const short4 nb = nbs[ec];
+        const double* uo = us + ec * SU;
+        const double* xyo = uxy + ec * SXY;
+        const double det = geos[ec * SG + 5];
+        const double* fq0 = fgs + ec;
+#pragma unroll
+        for (int q = 0; q < T::NQ; ++q) {
+          far[q] = fas[q] = fag[q] = 0.0;
+          const int it = itab[q];
+          if (it >= 0) {
+            const int f = it >> 24, kk = (it >> 16) & 255, i = it & 65535;
+            const int fl = (nb.w >> (4 * f)) & 15;
+            const int fp = fl & 3, bc = fl >> 2;
+            const int slot = (f == 0) ? nb.x : (f == 1) ? nb.y : nb.z;
+            const double* fq = fq0 + 5 * f * T::FGS;
+            const double nx = fq[0], ny = fq[T::FGS], sJ = fq[2 * T::FGS];
+            // boundary faces read the element's own trace and mirror it (R7):
+            // Dirichlet u+ = -u-, grad u+ = grad u-;  Neumann u+ = u-, grad u+ = -grad u-
+            const bool inner = (bc == 0);
+            const int ps = inner ? slot : ec;
+            const int ip = inner ? nidx[(2 * fp + ((f == 2) == (fp == 2))) * NFP + kk] : i;
+            const double* xyn = uxy + ps * SXY;
+            const double um = uo[i], upr = us[ps * SU + ip];
+            const double dnm = nx * xyo[i] + ny * xyo[NPN + i];
+            const double dpr = nx * xyn[ip] + ny * xyn[NPN + ip];  // n- . grad u+ (before mirroring)
+            const double detp = inner ? geos[slot * SG + 5] : 0.0;
+            const double tau = a.tau_c * sJ * fmax(det, detp);      // Eq. Ch2.PenaltyParameter, 1/h = sJ det
+            const double delta = ((bc == 1) ? -upr : upr) - um;     // paper jump
+            const double dnp = (bc == 2) ? -dpr : dpr;
+            far[q] = fq[3 * T::FGS] * delta;                        // 1/2 sJ (n.grad r) delta
+            fas[q] = fq[4 * T::FGS] * delta;                        // 1/2 sJ (n.grad s) delta
+            fag[q] = -sJ * (0.5 * (dnm + dnp) + tau * delta);       // surface flux (face mass in the GEMM)
+          }
+        }
+      }
+      // P3: Au = [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss; E^T] (+ lambda J u M)
       const int e = 8 * warp + (lane >> 2);
       double C[NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = 8 * nt + 2 * (lane & 3) + h;
-          double s = 0.0;
-          if (i < NP) {
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int nf = nodeface[2 * i + q];
-              if (nf >= 0) {
-                const int f = nf / NFP, kk = nf - f * NFP;
-                const double* g = gs + e * NF3 + f * NFP;
-#pragma unroll
-                for (int m = 0; m < NFP; ++m) s += m1d[kk * NFP + m] * g[m];
-              }
-            }
-          }
-          C[nt][h] = s;
-        }
-      }
-      // w_r, w_s straight from registers (K rows permuted on the host to match the C layout)
+      for (int nt = 0; nt < NT; ++nt) C[nt][0] = C[nt][1] = 0.0;
 #pragma unroll
       for (int c = 0; c < 2 * NT; ++c) {
         const double av = wr[c >> 1][c & 1];
@@ -378,16 +465,20 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
       }
-      const double* frow = fa + e * SF + (lane & 3);
 #pragma unroll
-      for (int kc = 0; kc < KCF; ++kc) {
-        const double av = frow[4 * kc];
-        const double* bt = tabM + (KCW + kc) * NT * 32 + lane;
+      for (int q = 0; q < T::NQ; ++q) {
+        const double* b0 = tabM + (KCW + q) * NT * 32 + lane;
+        const double* b1 = tabM + (KCW + T::NQ + q) * NT * 32 + lane;
+        const double* b2 = tabM + (KCW + 2 * T::NQ + q) * NT * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
+        for (int j = 0; j < NT; ++j) {
+          dmma(C[j][0], C[j][1], far[q], b0[j * 32]);
+          dmma(C[j][0], C[j][1], fas[q], b1[j * 32]);
+          dmma(C[j][0], C[j][1], fag[q], b2[j * 32]);
+        }
       }
       if (LAM) {
-        const double lj = a.lambda * geos[e * 5 + 4];
+        const double lj = a.lambda * geos[e * SG + 4];
         const double* urow = us + e * SU + (lane & 3);
 #pragma unroll
         for (int kc = 0; kc < KCM; ++kc) {
@@ -398,7 +489,6 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
         }
       }
       if (e < Eb) {
-        double* out = (MODE == MODE_AX) ? a.Au : a.Au;
         const int64_t base = (e0 + e) * NP;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -406,13 +496,14 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, 1) k_sipdg(AxArgs a, int gmax) 
           for (int h = 0; h < 2; ++h) {
             const int i = 8 * nt + 2 * (lane & 3) + h;
             if (i < NP) {
-              out[base + i] = C[nt][h];
+              a.Au[base + i] = C[nt][h];
               if (MODE == MODE_PCG_A) dot += us[e * SU + i] * C[nt][h];
             }
           }
       }
     }
   }
+  cp_async_wait_all();
   if (MODE == MODE_PCG_A) {
     double v[1] = {dot}, out[1];
     if (grid_reduce<1>(v, red, a.partials, a.counter, out)) {

@@ -41,8 +41,30 @@ def test_c1_unpreconditioned():
 @pytest.mark.parametrize("N", [1, 3, 4, 6, 8])
 def test_jacobi_mixed_boundaries(N):
     m = meshgen.square(10, jitter=0.2, diag="random", order="morton", seed=6,
-                       tag=lambda x, y: np.where(x > 0.95, 1, 2).astype(np.int8))
+                       tag=lambda x, y: np.where(y < 0.5, 1, 2).astype(np.int8))
     check_solve(m, N, 1, 1e-8, f=lambda x, y: np.exp(-((x - 0.3) ** 2 + y ** 2) / 0.1))
+
+
+@pytest.mark.parametrize("N", [6, 8])
+def test_jacobi_nearly_neumann_long_solve(N):
+    """Dirichlet only on the edge x = 1 (cylinder-like pressure problem): ~1700 iterations.
+
+    Over that many iterations the FMA contraction and the summation order of the GPU
+    reductions perturb CG's short recurrences at the rounding level, so the iteration count
+    may move by a few (reading R15); the solution is held to the oracle's residual."""
+    m = meshgen.square(10, jitter=0.2, diag="random", order="morton", seed=6,
+                       tag=lambda x, y: np.where(x > 0.95, 1, 2).astype(np.int8))
+    ref = RefElem(N)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    f = lambda x, y: np.exp(-((x - 0.3) ** 2 + y ** 2) / 0.1)  # noqa: E731
+    b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, f)
+    op = Ipdg(N, m)
+    x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-8, maxit=20000)
+    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-8, 20000, dinv=1.0 / A.diagonal())
+    assert st["status"] == sto["status"] == 0
+    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    r = b.ravel() - A @ x.cpu().numpy().ravel()
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b) * 1.05
 
 
 def test_screened_poisson_lambda():
