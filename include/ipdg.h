@@ -129,6 +129,26 @@ int ipdg_pcg_solve_host(ipdg_ctx ctx, const double* b_host, double* x_host, doub
  * IPDG_BC_REMOTE are then matched across ranks through the global vertex ids in EToV
  * (same vertex numbering on every rank), and the PCG dot products are all-reduced. */
 int ipdg_comm_init(ipdg_ctx ctx, const void* nccl_unique_id, int nranks, int rank);
+
+/* Complete a mesh uploaded with IPDG_BC_REMOTE faces (multi-GPU partition, built e.g. by
+ * paper_1801_00246_b200.partition.split).  HOST arrays, copied:
+ *   H              ghost elements owned by other ranks (local ids K .. K+H-1)
+ *   ghost_etov     [H*3] their global vertex ids (coordinates from the VX, VY of ipdg_upload_mesh)
+ *   remote         [K*3] ghost index h on IPDG_BC_REMOTE faces (else ignored)
+ *   remote_face    [K*3] the ghost's face index f' on those faces
+ *   nnbr, nbr_rank [nnbr] neighbour ranks; send_off/recv_off [nnbr+1] offsets;
+ *   send_elem      [send_off[nnbr]] local element ids sent to each neighbour, in the order the
+ *                  neighbour stores them as ghosts (its recv list from this rank).
+ * Every ipdg_ax / PCG iteration then exchanges the ghost rows with NCCL send/recv on the
+ * caller's stream before the operator kernel. */
+int ipdg_upload_halo(ipdg_ctx ctx, int64_t H, const int32_t* ghost_etov, const int32_t* remote,
+                     const int8_t* remote_face, int nnbr, const int32_t* nbr_rank, const int64_t* send_off,
+                     const int32_t* send_elem, const int64_t* recv_off);
+/* Halo introspection / single-process exchange (tests): S sent rows, H ghost rows; pack the
+ * S x Np rows of a field in plan order; install H x Np ghost rows (disables the NCCL exchange). */
+int ipdg_halo_info(ipdg_ctx ctx, int64_t* S, int64_t* H);
+int ipdg_halo_pack(ipdg_ctx ctx, const double* u, double* out, void* stream);
+int ipdg_halo_set(ipdg_ctx ctx, const double* in, void* stream);
 int ipdg_nccl_id_bytes(void);
 int ipdg_nccl_get_unique_id(void* out128);
 

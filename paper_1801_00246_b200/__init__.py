@@ -58,6 +58,54 @@ class Ipdg:
         except Exception:
             pass
 
+    @classmethod
+    def from_rank_mesh(cls, N, rm, device=0, tau_scale=1.0, nccl_id=None):
+        """Context for one partition (paper_1801_00246_b200.partition.RankMesh).
+
+        With nccl_id (bytes of an ncclUniqueId shared by all ranks) the halo is exchanged with NCCL;
+        without it the caller installs ghost rows with halo_set (single-process tests)."""
+        op = cls(N, device=device)
+        if nccl_id is not None:
+            op.comm_init(nccl_id, rm.nparts, rm.rank)
+        op.upload_mesh(rm.local_mesh(), tau_scale)
+        if rm.H > 0 or (rm.bc == 3).any():
+            ge = np.ascontiguousarray(rm.ghost_EToV, dtype=np.int32)
+            rem = np.ascontiguousarray(rm.remote, dtype=np.int32)
+            rf = np.ascontiguousarray(rm.remote_face, dtype=np.int8)
+            nr = np.ascontiguousarray(rm.nbr_ranks, dtype=np.int32)
+            so = np.ascontiguousarray(rm.send_off, dtype=np.int64)
+            se = np.ascontiguousarray(rm.send_elems, dtype=np.int32)
+            ro = np.ascontiguousarray(rm.recv_off, dtype=np.int64)
+            check(lib().ipdg_upload_halo(op.ctx, rm.H, ge.ctypes.data, rem.ctypes.data, rf.ctypes.data, nr.size,
+                                         nr.ctypes.data, so.ctypes.data, se.ctypes.data, ro.ctypes.data), op.ctx)
+        op.rank_mesh = rm
+        return op
+
+    @classmethod
+    def distributed(cls, N, mesh, part, rank, world, device=0, tau_scale=1.0):
+        """One rank of a torch.distributed job: partition, NCCL bootstrap (id broadcast), upload."""
+        import torch.distributed as dist
+        from . import partition
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rm = partition.split(mesh, part, world, ranks=[rank])[0]
+        return cls.from_rank_mesh(N, rm, device=device, tau_scale=tau_scale, nccl_id=obj[0])
+
+    def halo_info(self):
+        S, H = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().ipdg_halo_info(self.ctx, ctypes.byref(S), ctypes.byref(H)), self.ctx)
+        return S.value, H.value
+
+    def halo_pack(self, u, stream=None):
+        import torch
+        S, _ = self.halo_info()
+        out = torch.empty(max(S, 1), self.Np, dtype=torch.float64, device="cuda:%d" % self.device)
+        check(lib().ipdg_halo_pack(self.ctx, _ptr(u), _ptr(out), _stream(stream)), self.ctx)
+        return out[:S]
+
+    def halo_set(self, ghosts, stream=None):
+        check(lib().ipdg_halo_set(self.ctx, _ptr(ghosts.contiguous()), _stream(stream)), self.ctx)
+
     # ---- setup
     def comm_init(self, nccl_id_bytes, nranks, rank):
         buf = ctypes.create_string_buffer(bytes(nccl_id_bytes), len(nccl_id_bytes))
@@ -72,6 +120,7 @@ class Ipdg:
         check(lib().ipdg_upload_mesh(self.ctx, K, VX.size, VX.ctypes.data, VY.ctypes.data, EToV.ctypes.data,
                                      bc.ctypes.data, float(tau_scale)), self.ctx)
         self.K = K
+        self.rank_mesh = None
         self._ws = None
 
     def _workspace(self):

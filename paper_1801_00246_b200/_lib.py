@@ -49,6 +49,10 @@ SIGNATURES = {
     "ipdg_pcg_iterate_profiled": (_int, [_vp, _i64, _c.POINTER(_d), _c.POINTER(_d), _vp]),
     "ipdg_pcg_solve_host": (_int, [_vp, _vp, _vp, _d, _int, _d, _i64, _c.POINTER(ipdg_stats), _vp]),
     "ipdg_comm_init": (_int, [_vp, _vp, _int, _int]),
+    "ipdg_upload_halo": (_int, [_vp, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
+    "ipdg_halo_info": (_int, [_vp, _c.POINTER(_i64), _c.POINTER(_i64)]),
+    "ipdg_halo_pack": (_int, [_vp, _vp, _vp, _vp]),
+    "ipdg_halo_set": (_int, [_vp, _vp, _vp]),
     "ipdg_nccl_id_bytes": (_int, []),
     "ipdg_nccl_get_unique_id": (_int, [_vp]),
     "ipdg_get_refop": (_int, [_vp, _int, _vp, _i64]),

@@ -79,6 +79,20 @@ struct ipdg_ctx_s {
   double gkey_lambda = -1.0;
   int gkey_precond = -1;
   cudaStream_t cap_stream = nullptr;
+  // pending host mesh (ipdg_upload_mesh -> ipdg_upload_halo)
+  int64_t pend_K = 0, pend_remote = 0;
+  std::vector<int> pend_etoe, pend_etof;
+  std::vector<int8_t> pend_bc;
+  std::vector<double> pend_vxy, pend_VX, pend_VY;
+  // halo (multi-GPU): S sent element rows, H received ghost rows
+  int64_t S = 0;
+  int* send_idx = nullptr;
+  double* sendbuf = nullptr;
+  double* halobuf = nullptr;
+  std::vector<int> nbr_rank;
+  std::vector<int64_t> send_off, recv_off;
+  bool has_dirichlet_global = false;
+  bool halo_external = false;  // caller fills the halo buffer (ipdg_halo_set), no NCCL
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -258,6 +272,7 @@ struct Impl {
     a.boff = c->boff;
     a.tables = c->tables;
     a.tau_c = c->tau_c;
+    a.halo_p = c->halobuf;
     return a;
   }
 
@@ -397,6 +412,11 @@ static void free_mesh(ipdg_ctx c) {
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   c->gkey_x = nullptr;
   c->dinv_valid = false;
+  if (c->send_idx) cudaFree(c->send_idx);
+  if (c->sendbuf) cudaFree(c->sendbuf);
+  if (c->halobuf) cudaFree(c->halobuf);
+  c->send_idx = nullptr; c->sendbuf = nullptr; c->halobuf = nullptr;
+  c->S = 0; c->H = 0; c->K = 0; c->halo_external = false;
 }
 
 static void free_ws(ipdg_ctx c) {
@@ -498,6 +518,8 @@ int ipdg_destroy(ipdg_ctx c) {
   return IPDG_OK;
 }
 
+static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy);
+
 int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const double* VY, const int32_t* EToV,
                      const int8_t* bc, double tau_scale) {
   if (!c) return IPDG_EINVAL;
@@ -530,29 +552,55 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
     i = j;
   }
   bool dir = false;
+  int64_t nremote = 0;
   for (int64_t i = 0; i < K * 3; ++i) {
     if (bc[i] == IPDG_BC_INTERIOR && etoe[i] < 0) FAIL(c, IPDG_EMESH, "interior face (%lld,%lld) has no neighbour", (long long)(i / 3), (long long)(i % 3));
     if (bc[i] != IPDG_BC_INTERIOR && etoe[i] >= 0) FAIL(c, IPDG_EMESH, "boundary-coded face (%lld,%lld) has a neighbour", (long long)(i / 3), (long long)(i % 3));
-    if (bc[i] == IPDG_BC_REMOTE) FAIL(c, IPDG_EINVAL, "remote faces need ipdg_comm_init (multi-GPU)");
     if (bc[i] == IPDG_BC_DIRICHLET) dir = true;
+    if (bc[i] == IPDG_BC_REMOTE) ++nremote;
   }
   c->has_dirichlet = dir;
+  c->pend_K = K;
+  c->pend_etoe = std::move(etoe);
+  c->pend_etof = std::move(etof);
+  c->pend_bc.assign(bc, bc + K * 3);
+  c->pend_vxy.resize(K * 6);
+  for (int64_t e = 0; e < K; ++e)
+    for (int v = 0; v < 3; ++v) {
+      c->pend_vxy[e * 6 + 2 * v] = VX[EToV[e * 3 + v]];
+      c->pend_vxy[e * 6 + 2 * v + 1] = VY[EToV[e * 3 + v]];
+    }
+  c->pend_VX.assign(VX, VX + Nv);
+  c->pend_VY.assign(VY, VY + Nv);
+  c->tau_c = 0.5 * (c->N + 1) * (c->N + 2) * tau_scale;
+  c->pend_remote = nremote;
+  if (nremote > 0) return IPDG_OK;  // completed by ipdg_upload_halo
+  return finalize_mesh(c, 0, nullptr);
+}
+
+// Block schedule, device arrays, geometric factors and launch configuration for the mesh
+// stored by ipdg_upload_mesh plus H halo ghosts (ghost element g has local id K + g).
+static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
+  const int64_t K = c->pend_K;
+  const int E = c->E;
+  std::vector<int>& etoe = c->pend_etoe;
+  std::vector<int>& etof = c->pend_etof;
+  const int8_t* bc = c->pend_bc.data();
   // ---- element blocks and ghost lists.  A block is a contiguous range of at most E own
   // elements whose distinct outside face neighbours (ghosts) fit the shared-memory budget
   // gcap; well-ordered meshes (Morton, RCB) never hit the cap, scattered orderings get
-  // shorter blocks instead of failing.
-  const int gcap = ghost_cap(c->N, c->sms > 0 ? c->device : 0);
+  // shorter blocks instead of failing.  Halo ghosts (id >= K) are ordinary ghosts whose
+  // values come from the received halo buffer.
+  const int gcap = ghost_cap(c->N, c->device);
   std::vector<int> goff(1, 0), gid, boff(1, 0);
   std::vector<short4> nbr(K);
   int gmax = 0;
   std::vector<int> gl;
   int64_t e0 = 0;
   while (e0 < K) {
-    // grow the block greedily
     gl.clear();
     int64_t e1 = e0;
     while (e1 < K && e1 - e0 < E) {
-      size_t before = gl.size();
       for (int f = 0; f < 3; ++f) {
         const int n = etoe[e1 * 3 + f];
         if (n >= 0 && (n < e0 || n > e1)) gl.push_back(n);
@@ -562,7 +610,6 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
       // neighbours inside [e0, e1] are own elements: drop them from the ghost list
       gl.erase(std::remove_if(gl.begin(), gl.end(), [&](int n) { return n >= e0 && n <= e1; }), gl.end());
       if ((int)gl.size() > gcap && e1 > e0) {  // roll back this element
-        gl.resize(before);
         gl.clear();
         for (int64_t e = e0; e < e1; ++e)
           for (int f = 0; f < 3; ++f) {
@@ -588,7 +635,8 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
         }
         sl[f] = (short)slot;
         const int fp = n >= 0 ? etof[e * 3 + f] : 0;
-        flags |= ((fp & 3) | ((bc[e * 3 + f] & 3) << 2)) << (4 * f);
+        const int code = (bc[e * 3 + f] == IPDG_BC_REMOTE) ? IPDG_BC_INTERIOR : bc[e * 3 + f];
+        flags |= ((fp & 3) | ((code & 3) << 2)) << (4 * f);
       }
       nbr[e] = make_short4(sl[0], sl[1], sl[2], (short)flags);
     }
@@ -600,15 +648,11 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
   const int nb = (int)boff.size() - 1;
   if (E + gmax > 32000) FAIL(c, IPDG_EMESH, "element ordering too scattered (a block has %d ghosts)", gmax);
   c->K = K;
+  c->H = H;
   c->nblocks = nb;
   c->gmax = gmax;
-  c->tau_c = 0.5 * (c->N + 1) * (c->N + 2) * tau_scale;
-  std::vector<double> vxy(K * 6);
-  for (int64_t e = 0; e < K; ++e)
-    for (int v = 0; v < 3; ++v) {
-      vxy[e * 6 + 2 * v] = VX[EToV[e * 3 + v]];
-      vxy[e * 6 + 2 * v + 1] = VY[EToV[e * 3 + v]];
-    }
+  std::vector<double> vxy(c->pend_vxy);
+  if (H > 0) vxy.insert(vxy.end(), ghost_vxy, ghost_vxy + H * 6);
   std::vector<int8_t> bcv(bc, bc + K * 3);
   TRY(upload(c, &c->vxy, vxy.data(), vxy.size()));
   TRY(upload(c, &c->nbr, nbr.data(), nbr.size()));
@@ -619,12 +663,13 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
   TRY(upload(c, &c->bcode, bcv.data(), bcv.size()));
   c->etoe_h = etoe;
   c->etof_h = etof;
-  CUDA_TRY(c, cudaMalloc(&c->geo, K * sizeof(double4)));
+  const int64_t KH = K + H;
+  CUDA_TRY(c, cudaMalloc(&c->geo, KH * sizeof(double4)));
   unsigned long long* bad = nullptr;
   CUDA_TRY(c, cudaMalloc(&bad, sizeof(unsigned long long)));
   const unsigned long long none = ~0ull;
   CUDA_TRY(c, cudaMemcpy(bad, &none, sizeof(none), cudaMemcpyHostToDevice));
-  k_geometry<<<(unsigned)((K + 255) / 256), 256>>>(K, c->vxy, c->geo, bad);
+  k_geometry<<<(unsigned)((KH + 255) / 256), 256>>>(KH, c->vxy, c->geo, bad);
   c->launches++;
   unsigned long long badh = none;
   CUDA_TRY(c, cudaMemcpy(&badh, bad, sizeof(badh), cudaMemcpyDeviceToHost));
@@ -633,9 +678,143 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
   DISPATCH(c->N, configure(c));
 }
 
+int ipdg_upload_halo(ipdg_ctx c, int64_t H, const int32_t* ghost_etov, const int32_t* remote, const int8_t* remote_face,
+                     int nnbr, const int32_t* nbr_rank, const int64_t* send_off, const int32_t* send_elem,
+                     const int64_t* recv_off) {
+  if (!c || H < 0 || nnbr < 0 || (H > 0 && (!ghost_etov || !remote || !remote_face)) ||
+      (nnbr > 0 && (!nbr_rank || !send_off || !send_elem || !recv_off)))
+    FAIL(c, IPDG_EINVAL, "upload_halo: bad arguments");
+  if (c->pend_K == 0 || c->pend_remote == 0) FAIL(c, IPDG_ESTATE, "upload_halo needs a mesh with IPDG_BC_REMOTE faces");
+  const int64_t K = c->pend_K, Nv = (int64_t)c->pend_VX.size();
+  if (recv_off[nnbr] != H) FAIL(c, IPDG_EINVAL, "upload_halo: receive offsets do not cover H ghosts");
+  for (int64_t i = 0; i < K * 3; ++i) {
+    if (c->pend_bc[i] != IPDG_BC_REMOTE) continue;
+    const int h = remote[i], fp = remote_face[i];
+    if (h < 0 || h >= H || fp < 0 || fp > 2) FAIL(c, IPDG_EMESH, "remote face %lld has no valid ghost", (long long)i);
+    c->pend_etoe[i] = (int)(K + h);
+    c->pend_etof[i] = fp;
+  }
+  std::vector<double> gv(H * 6);
+  for (int64_t g = 0; g < H; ++g)
+    for (int v = 0; v < 3; ++v) {
+      const int64_t id = ghost_etov[g * 3 + v];
+      if (id < 0 || id >= Nv) FAIL(c, IPDG_EMESH, "ghost %lld has an invalid vertex id", (long long)g);
+      gv[g * 6 + 2 * v] = c->pend_VX[id];
+      gv[g * 6 + 2 * v + 1] = c->pend_VY[id];
+    }
+  c->nbr_rank.assign(nbr_rank, nbr_rank + nnbr);
+  c->send_off.assign(send_off, send_off + nnbr + 1);
+  c->recv_off.assign(recv_off, recv_off + nnbr + 1);
+  const int64_t S = nnbr ? send_off[nnbr] : 0;
+  TRY(upload(c, &c->send_idx, send_elem, (size_t)S));
+  c->S = S;
+  if (c->sendbuf) cudaFree(c->sendbuf);
+  if (c->halobuf) cudaFree(c->halobuf);
+  c->sendbuf = c->halobuf = nullptr;
+  CUDA_TRY(c, cudaMalloc(&c->sendbuf, std::max<int64_t>(1, S) * c->ref.Np * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->halobuf, std::max<int64_t>(1, H) * c->ref.Np * sizeof(double)));
+  CUDA_TRY(c, cudaMemset(c->halobuf, 0, std::max<int64_t>(1, H) * c->ref.Np * sizeof(double)));
+  // a Dirichlet face on any rank makes the operator non-singular
+  if (c->comm && c->nranks > 1) {
+    double* flag = nullptr;
+    CUDA_TRY(c, cudaMalloc(&flag, sizeof(double)));
+    const double v = c->has_dirichlet ? 1.0 : 0.0;
+    CUDA_TRY(c, cudaMemcpy(flag, &v, sizeof(v), cudaMemcpyHostToDevice));
+    NCCL_TRY(c, ncclAllReduce(flag, flag, 1, ncclFloat64, ncclSum, c->comm, 0));
+    double g = 0.0;
+    CUDA_TRY(c, cudaMemcpy(&g, flag, sizeof(g), cudaMemcpyDeviceToHost));
+    cudaFree(flag);
+    c->has_dirichlet_global = g > 0.0;
+  } else {
+    c->has_dirichlet_global = c->has_dirichlet;
+  }
+  return finalize_mesh(c, H, gv.data());
+}
+
+// ---- halo exchange (multi-GPU): pack the rows other ranks need, NCCL send/recv into the halo buffer
+__global__ void k_pack_rows(int64_t S, int NP, const int* __restrict__ idx, const double* __restrict__ u,
+                            double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= S * NP) return;
+  const int64_t s = t / NP;
+  const int i = (int)(t - s * NP);
+  out[t] = u[(int64_t)idx[s] * NP + i];
+}
+
+// p_k = D^-1 r + beta p_{k-1} at the send rows, with the same decisions as pass A's prologue
+__global__ void k_pack_p(int64_t S, int NP, const int* __restrict__ idx, const double* __restrict__ r,
+                         const double* __restrict__ dinv, const double* p_even, const double* p_odd,
+                         const PcgState* st, double* __restrict__ out) {
+  if (st->stop_iter >= 0) return;
+  const long long k = st->it + 1;
+  const bool first = (k == 1);
+  const double beta = first ? 0.0 : st->red_B[0] / st->rho_hist[(k - 2) & 3];
+  const double* pold = (k & 1) ? p_even : p_odd;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= S * NP) return;
+  const int64_t s = t / NP;
+  const int i = (int)(t - s * NP);
+  const int64_t g = (int64_t)idx[s] * NP + i;
+  const double z = dinv ? r[g] * dinv[g] : r[g];
+  out[t] = first ? z : z + beta * pold[g];
+}
+
+static int halo_exchange(ipdg_ctx c, cudaStream_t s) {
+  const int NP = c->ref.Np;
+  NCCL_TRY(c, ncclGroupStart());
+  for (size_t j = 0; j < c->nbr_rank.size(); ++j) {
+    const int64_t so = c->send_off[j], sn = c->send_off[j + 1] - so;
+    const int64_t ro = c->recv_off[j], rn = c->recv_off[j + 1] - ro;
+    if (sn) NCCL_TRY(c, ncclSend(c->sendbuf + so * NP, sn * NP, ncclFloat64, c->nbr_rank[j], c->comm, s));
+    if (rn) NCCL_TRY(c, ncclRecv(c->halobuf + ro * NP, rn * NP, ncclFloat64, c->nbr_rank[j], c->comm, s));
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  return IPDG_OK;
+}
+
+static int halo_for_field(ipdg_ctx c, const double* u, cudaStream_t s) {
+  if (c->H == 0 && c->S == 0) return IPDG_OK;
+  if (c->halo_external) return IPDG_OK;  // test mode: the caller filled the halo buffer
+  if (!c->comm) FAIL(c, IPDG_ESTATE, "mesh has remote faces but no communicator (ipdg_comm_init)");
+  const int64_t n = c->S * c->ref.Np;
+  if (n) {
+    k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, u, c->sendbuf);
+    c->launches++;
+  }
+  return halo_exchange(c, s);
+}
+
+int ipdg_halo_info(ipdg_ctx c, int64_t* S, int64_t* H) {
+  if (!c || !S || !H) return IPDG_EINVAL;
+  *S = c->S;
+  *H = c->H;
+  return IPDG_OK;
+}
+
+int ipdg_halo_pack(ipdg_ctx c, const double* u, double* out, void* stream) {
+  if (!c || !u || !out) return IPDG_EINVAL;
+  const int64_t n = c->S * c->ref.Np;
+  if (n) {
+    k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(c->S, c->ref.Np, c->send_idx, u, out);
+    c->launches++;
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+int ipdg_halo_set(ipdg_ctx c, const double* in, void* stream) {
+  if (!c || !in) return IPDG_EINVAL;
+  if (c->H == 0) FAIL(c, IPDG_ESTATE, "no halo");
+  CUDA_TRY(c, cudaMemcpyAsync(c->halobuf, in, c->H * c->ref.Np * sizeof(double), cudaMemcpyDeviceToDevice,
+                              (cudaStream_t)stream));
+  c->halo_external = true;
+  return IPDG_OK;
+}
+
 int ipdg_ax(ipdg_ctx c, const double* u, double* Au, double lambda, void* stream) {
   if (!c || !u || !Au || u == Au || !(lambda >= 0.0)) return c ? (c->err = "ipdg_ax: bad arguments", IPDG_EINVAL) : IPDG_EINVAL;
-  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_ax before ipdg_upload_mesh");
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_ax before ipdg_upload_mesh (or ipdg_upload_halo)");
+  TRY(halo_for_field(c, u, (cudaStream_t)stream));
   DISPATCH(c->N, ax(c, u, Au, lambda, (cudaStream_t)stream));
 }
 
@@ -723,7 +902,20 @@ static int allreduce(ipdg_ctx c, double* buf, int n, cudaStream_t s) {
 
 static int vec_grid(ipdg_ctx c) { return std::min(c->sms * 8, 4096); }
 
+static int halo_for_p(ipdg_ctx c, cudaStream_t s) {
+  if (c->H == 0 && c->S == 0) return IPDG_OK;
+  if (!c->comm) FAIL(c, IPDG_ESTATE, "distributed PCG needs a communicator (ipdg_comm_init)");
+  const int64_t n = c->S * c->ref.Np;
+  if (n) {
+    k_pack_p<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, c->r,
+                                                         c->precond ? c->dinv : nullptr, c->pe, c->po, c->st, c->sendbuf);
+    c->launches++;
+  }
+  return halo_exchange(c, s);
+}
+
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
+  TRY(halo_for_p(c, s));
   TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
   TRY(allreduce(c, &c->st->red_A, 1, s));
   k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->st,
@@ -754,12 +946,8 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
 int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, void* stream) {
   if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || (precond != 0 && precond != 1)) return IPDG_EINVAL;
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
-  if (lambda == 0.0 && !c->has_dirichlet) {
-    int any = 0;
-    // multi-GPU: a Dirichlet face on any rank makes the operator non-singular
-    if (c->comm && c->nranks > 1) any = -1;
-    if (any == 0) FAIL(c, IPDG_ESINGULAR, "lambda = 0 and no Dirichlet face");
-  }
+  const bool dir = (c->H > 0 || c->S > 0) ? c->has_dirichlet_global : c->has_dirichlet;
+  if (lambda == 0.0 && !dir) FAIL(c, IPDG_ESINGULAR, "lambda = 0 and no Dirichlet face");
   cudaStream_t s = (cudaStream_t)stream;
   TRY(ensure_ws(c));
   TRY(ensure_partials(c));
@@ -835,6 +1023,7 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b,
     const int m = (int)std::min<int64_t>(n, B);
     for (int i = 0; i < m && rc == IPDG_OK; ++i) {
       cudaEventRecord(ev[3 * i], s);
+      if ((rc = halo_for_p(c, s)) != IPDG_OK) break;
       rc = [&]() -> int { DISPATCH(c->N, pass_a(c, s)); }();
       if (rc != IPDG_OK) break;
       if ((rc = allreduce(c, &c->st->red_A, 1, s)) != IPDG_OK) break;
