@@ -59,7 +59,7 @@ struct SmemLayout {
     L.us = o; o += slots * T::SU;
     o = (o + 1) & ~1;
     L.geo = o; o += slots * T::SG;
-    L.fg = o; o += 15 * T::FGS;        // own elements: per face n_x n_y sJ c_r c_s, layout [5f + field][e]
+    L.fg = o; o += 9 * T::FGS;         // own elements: per face c_r c_s sJ*tau, layout [3f + field][e]
     L.nb = o; o += 2 * T::E;            // short4 per element, double-buffered
     L.gid = o; o += gm8;                // 2 x gm8 ints, double-buffered
     o = (o + 1) & ~1;
@@ -373,31 +373,40 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
       const double det = rx * sy - sx * ry;  // = 1/J
       const double J = 1.0 / det;
       if ((lane & 3) == 0) { gq[4] = J; gq[5] = det; }
-      if (own && (lane & 3) < 3) {  // one face per lane: unit normal, sJ, lift coefficients
+      if (own && (lane & 3) < 3 && srow < Eb) {  // one face per lane: lift coefficients and sJ * tau
         const int f = lane & 3;
         const double gx = (f == 0) ? -sx : (f == 1) ? rx + sx : -rx;  // outward: -grad s, grad r+s, -grad r
         const double gy = (f == 0) ? -sy : (f == 1) ? ry + sy : -ry;
-        const double len = sqrt(gx * gx + gy * gy);
-        const double il = 1.0 / len;
-        double* fq = fgs + 5 * f * T::FGS + srow;
-        fq[0] = gx * il;
-        fq[T::FGS] = gy * il;
-        fq[2 * T::FGS] = J * len;                        // sJ = edge length / 2 (R6)
-        fq[3 * T::FGS] = 0.5 * J * (rx * gx + ry * gy);  // 1/2 sJ (n . grad r)
-        fq[4 * T::FGS] = 0.5 * J * (sx * gx + sy * gy);  // 1/2 sJ (n . grad s)
+        const double sJ = J * sqrt(gx * gx + gy * gy);                 // edge length / 2 (R6)
+        const short4 nb = nbs[srow];
+        const int bc = (nb.w >> (4 * f + 2)) & 3;
+        double detp = 0.0;                                             // neighbour det G (= 1/J+) on interior faces
+        if (bc == 0) {
+          const double* gn = geos + ((f == 0) ? nb.x : (f == 1) ? nb.y : nb.z) * SG;
+          detp = gn[0] * gn[3] - gn[1] * gn[2];
+        }
+        double* fq = fgs + 3 * f * T::FGS + srow;
+        fq[0] = 0.5 * J * (rx * gx + ry * gy);                          // 1/2 sJ (n . grad r)
+        fq[T::FGS] = 0.5 * J * (sx * gx + sy * gy);                     // 1/2 sJ (n . grad s)
+        fq[2 * T::FGS] = sJ * a.tau_c * sJ * fmax(det, detp);           // sJ tau, Eq. Ch2.PenaltyParameter (1/h = sJ/J)
       }
+      // w_r = J (G_rr u_r + G_rs u_s), w_s = J (G_rs u_r + G_ss u_s).  They are also the scaled
+      // normal derivatives at the face nodes: J g_f . grad u with g_f = -grad s, grad r + grad s,
+      // -grad r gives sJ (n . grad u) = -w_s, w_r + w_s, -w_r on faces 0, 1, 2.
       const double Grr = J * (rx * rx + ry * ry), Grs = J * (rx * sx + ry * sy), Gss = J * (sx * sx + sy * sy);
-      double* xyrow = uxy + srow * SXY + 2 * (lane & 3);
+      double* wrow = uxy + srow * SXY + 2 * (lane & 3);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const double ur0 = acc[nt][0], ur1 = acc[nt][1], us0 = acc[NT + nt][0], us1 = acc[NT + nt][1];
-        *reinterpret_cast<double2*>(xyrow + 8 * nt) = make_double2(rx * ur0 + sx * us0, rx * ur1 + sx * us1);
-        *reinterpret_cast<double2*>(xyrow + NPN + 8 * nt) = make_double2(ry * ur0 + sy * us0, ry * ur1 + sy * us1);
+        const double r0 = Grr * ur0 + Grs * us0, r1 = Grr * ur1 + Grs * us1;
+        const double s0 = Grs * ur0 + Gss * us0, s1 = Grs * ur1 + Gss * us1;
+        *reinterpret_cast<double2*>(wrow + 8 * nt) = make_double2(r0, r1);
+        *reinterpret_cast<double2*>(wrow + NPN + 8 * nt) = make_double2(s0, s1);
         if (own) {
-          wr[nt][0] = Grr * ur0 + Grs * us0;
-          wr[nt][1] = Grr * ur1 + Grs * us1;
-          ws[nt][0] = Grs * ur0 + Gss * us0;
-          ws[nt][1] = Grs * ur1 + Gss * us1;
+          wr[nt][0] = r0;
+          wr[nt][1] = r1;
+          ws[nt][0] = s0;
+          ws[nt][1] = s1;
         }
       }
     }
@@ -413,8 +422,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
         const int ec = e < Eb ? e : 8 * warp;  // rows past the block end compute on a valid slot, never stored
         const short4 nb = nbs[ec];
         const double* uo = us + ec * SU;
-        const double* xyo = uxy + ec * SXY;
-        const double det = geos[ec * SG + 5];
+        const double* wo = uxy + ec * SXY;
         const double* fq0 = fgs + ec;
 #pragma unroll
         for (int q = 0; q < T::NQ; ++q) {
@@ -425,24 +433,25 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
             const int fl = (nb.w >> (4 * f)) & 15;
             const int fp = fl & 3, bc = fl >> 2;
             const int slot = (f == 0) ? nb.x : (f == 1) ? nb.y : nb.z;
-            const double* fq = fq0 + 5 * f * T::FGS;
-            const double nx = fq[0], ny = fq[T::FGS], sJ = fq[2 * T::FGS];
+            const double* fq = fq0 + 3 * f * T::FGS;
             // boundary faces read the element's own trace and mirror it (R7):
             // Dirichlet u+ = -u-, grad u+ = grad u-;  Neumann u+ = u-, grad u+ = -grad u-
             const bool inner = (bc == 0);
             const int ps = inner ? slot : ec;
+            const int pf = inner ? fp : f;
             const int ip = inner ? nidx[(2 * fp + ((f == 2) == (fp == 2))) * NFP + kk] : i;
-            const double* xyn = uxy + ps * SXY;
+            const double* wn = uxy + ps * SXY;
             const double um = uo[i], upr = us[ps * SU + ip];
-            const double dnm = nx * xyo[i] + ny * xyo[NPN + i];
-            const double dpr = nx * xyn[ip] + ny * xyn[NPN + ip];  // n- . grad u+ (before mirroring)
-            const double detp = inner ? geos[slot * SG + 5] : 0.0;
-            const double tau = a.tau_c * sJ * fmax(det, detp);      // Eq. Ch2.PenaltyParameter, 1/h = sJ det
+            // sJ n.grad u at the node: -w_s, w_r + w_s, -w_r on faces 0, 1, 2 (own normal for u-,
+            // the neighbour's own normal for u+, hence the sign flip below)
+            const double wro = wo[i], wso = wo[NPN + i], wrn = wn[ip], wsn = wn[NPN + ip];
+            const double tm = (f == 0) ? -wso : (f == 1) ? wro + wso : -wro;
+            const double tp = (pf == 0) ? -wsn : (pf == 1) ? wrn + wsn : -wrn;
+            const double tq = (bc == 1) ? tp : -tp;                 // sJ n-.grad u+ after mirroring
             const double delta = ((bc == 1) ? -upr : upr) - um;     // paper jump
-            const double dnp = (bc == 2) ? -dpr : dpr;
-            far[q] = fq[3 * T::FGS] * delta;                        // 1/2 sJ (n.grad r) delta
-            fas[q] = fq[4 * T::FGS] * delta;                        // 1/2 sJ (n.grad s) delta
-            fag[q] = -sJ * (0.5 * (dnm + dnp) + tau * delta);       // surface flux (face mass in the GEMM)
+            far[q] = fq[0] * delta;                                 // 1/2 sJ (n.grad r) delta
+            fas[q] = fq[T::FGS] * delta;                            // 1/2 sJ (n.grad s) delta
+            fag[q] = -0.5 * (tm + tq) - fq[2 * T::FGS] * delta;     // -sJ (n.{grad u} + tau delta)
           }
         }
       }
