@@ -227,6 +227,10 @@ class Ipdg:
         keys = ["N", "Np", "K", "nblocks", "E", "gmax", "smem_bytes", "grid"]
         return dict(zip(keys, list(out)))
 
+    def set_variant(self, variant):
+        """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux)."""
+        check(lib().ipdg_set_variant(self.ctx, int(variant)), self.ctx)
+
     def launch_count(self):
         return int(lib().ipdg_launch_count(self.ctx))
 

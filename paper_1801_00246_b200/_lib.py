@@ -61,6 +61,7 @@ SIGNATURES = {
     "ipdg_get_connectivity": (_int, [_vp, _vp, _vp, _i64]),
     "ipdg_info": (_int, [_vp, _c.POINTER(_i64), _int]),
     "ipdg_launch_count": (_i64, [_vp]),
+    "ipdg_set_variant": (_int, [_vp, _int]),
     "ipdg_strerror": (_c.c_char_p, [_int]),
     "ipdg_last_error": (_int, [_vp, _c.c_char_p, _int]),
 }

@@ -31,6 +31,7 @@
 #include "../../include/ipdg.h"
 #include "refops.h"
 #include "sipdg_kernels.cuh"
+#include "sipdg_split.cuh"
 
 using namespace ipdg;
 
@@ -55,6 +56,12 @@ struct ipdg_ctx_s {
   double* diagtab = nullptr;
   int nblocks = 0, gmax = 0;
   int E = 0;
+  // split variant (k_grad + k_flux): neighbour ids per element, W = [w_r | w_s] scratch
+  int4* nbg = nullptr;
+  double* W2 = nullptr;
+  int variant = 0;  // 0 auto (split for N >= 6), 1 fused, 2 split
+  size_t smem_grad = 0, smem_flux[2] = {0, 0};
+  int grid_grad = 0, grid_flux[2][2] = {{0, 0}, {0, 0}};
   size_t smem[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
   int grid[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
   // host copies for introspection
@@ -118,6 +125,12 @@ static constexpr int kChunk = 32;
   do {                                                                                             \
     ncclResult_t r_ = (x);                                                                         \
     if (r_ != ncclSuccess) FAIL(ctx, IPDG_ENCCL, "%s: %s", #x, ncclGetErrorString(r_));            \
+  } while (0)
+
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != IPDG_OK) return rc_; \
   } while (0)
 
 // ------------------------------------------------------------------ per-N dispatch
@@ -199,6 +212,25 @@ struct Impl {
     const size_t base = tab.size();
     tab.resize(base + ia.size() / 2);
     std::memcpy(tab.data() + base, ia.data(), ia.size() * sizeof(int));
+    // split variant (k_flux): main table with w_r, w_s rows in natural node order
+    using S = TrS<N>;
+    tab.resize(S::OFF_M2, 0.0);
+    tm = tab.data() + T::TAB_G;  // the vector may have moved
+    std::vector<double> m2(S::TAB_M2, 0.0);
+    for (int c = 0; c < S::KCW2 + T::KCF; ++c)
+      for (int j = 0; j < NT; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int n = 8 * j + (l >> 2);
+          double v;
+          if (c < S::KCW2) {
+            const int k = 4 * (c % T::KCG) + (l & 3);
+            v = at(c < T::KCG ? R.Sr : R.Ss, NP, k, n, NP, NP);
+          } else {
+            v = tm[((c - S::KCW2 + T::KCW) * NT + j) * 32 + l];  // face chunks: same as the fused table
+          }
+          m2[(c * NT + j) * 32 + l] = v;
+        }
+    tab.insert(tab.end(), m2.begin(), m2.end());
     return tab;
   }
 
@@ -257,6 +289,96 @@ struct Impl {
         c->grid[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
       }
     }
+    // split variant
+    using S = TrS<N>;
+    {
+      const size_t bytes = (size_t)(T::TAB_G + S::W * 8 * T::SU) * sizeof(double);
+      c->smem_grad = bytes;
+      const void* fns[2] = {(const void*)k_grad<N, MODE_AX>, (const void*)k_grad<N, MODE_PCG_A>};
+      int occ = 1;
+      for (const void* fn : fns) {
+        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        int o = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, S::W * 32, bytes));
+        occ = std::max(1, o);
+      }
+      const int64_t tiles = (c->K + c->H + 7) / 8;
+      c->grid_grad = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)occ * c->sms));
+    }
+    for (int lam = 0; lam < 2; ++lam) {
+      const size_t bytes = (size_t)(S::TAB_M2 + (lam ? T::TAB_L : 0)) * sizeof(double);
+      c->smem_flux[lam] = bytes;
+      for (int mode = 0; mode < 2; ++mode) {
+        const void* fn = (mode == 0) ? (lam ? (const void*)k_flux<N, MODE_AX, true> : (const void*)k_flux<N, MODE_AX, false>)
+                                     : (lam ? (const void*)k_flux<N, MODE_PCG_A, true> : (const void*)k_flux<N, MODE_PCG_A, false>);
+        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        int o = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, S::W * 32, bytes));
+        const int64_t tiles = (c->K + 7) / 8;
+        c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
+      }
+    }
+    return IPDG_OK;
+  }
+
+  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
+
+  static SplitArgs sargs(ipdg_ctx c) {
+    SplitArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.K = c->K;
+    a.H = c->H;
+    a.geo = c->geo;
+    a.nbg = c->nbg;
+    a.tables = c->tables;
+    a.tau_c = c->tau_c;
+    a.halo = c->halobuf;
+    a.W2 = c->W2;
+    return a;
+  }
+
+  static int ensure_w2(ipdg_ctx c) {
+    if (c->W2) return IPDG_OK;
+    CUDA_TRY(c, cudaMalloc(&c->W2, std::max<int64_t>(1, c->K + c->H) * 2 * T::NP * sizeof(double)));
+    return IPDG_OK;
+  }
+
+  static int ax_split(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
+    TRY(ensure_w2(c));
+    SplitArgs a = sargs(c);
+    a.W2 = c->W2;
+    a.u = u;
+    a.Au = Au;
+    a.lambda = lambda;
+    using S = TrS<N>;
+    k_grad<N, MODE_AX><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+    if (lambda != 0.0) k_flux<N, MODE_AX, true><<<c->grid_flux[0][1], S::W * 32, c->smem_flux[1], s>>>(a);
+    else k_flux<N, MODE_AX, false><<<c->grid_flux[0][0], S::W * 32, c->smem_flux[0], s>>>(a);
+    c->launches += 2;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
+  static int pass_a_split(ipdg_ctx c, cudaStream_t s) {
+    TRY(ensure_w2(c));
+    SplitArgs a = sargs(c);
+    a.W2 = c->W2;
+    a.lambda = c->lambda;
+    a.r = c->r;
+    a.dinv = c->precond ? c->dinv : nullptr;
+    a.p_even = c->pe;
+    a.p_odd = c->po;
+    a.x = c->x;
+    a.Au = c->Ap;
+    a.st = c->st;
+    a.partials = c->partials;
+    a.counter = c->counter;
+    using S = TrS<N>;
+    k_grad<N, MODE_PCG_A><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+    if (c->lambda != 0.0) k_flux<N, MODE_PCG_A, true><<<c->grid_flux[1][1], S::W * 32, c->smem_flux[1], s>>>(a);
+    else k_flux<N, MODE_PCG_A, false><<<c->grid_flux[1][0], S::W * 32, c->smem_flux[0], s>>>(a);
+    c->launches += 2;
+    CUDA_TRY(c, cudaGetLastError());
     return IPDG_OK;
   }
 
@@ -277,6 +399,7 @@ struct Impl {
   }
 
   static int ax(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
+    if (use_split(c)) return ax_split(c, u, Au, lambda, s);
     AxArgs a = args(c);
     a.u = u;
     a.Au = Au;
@@ -291,6 +414,7 @@ struct Impl {
   }
 
   static int pass_a(ipdg_ctx c, cudaStream_t s) {
+    if (use_split(c)) return pass_a_split(c, s);
     AxArgs a = args(c);
     a.lambda = c->lambda;
     a.r = c->r;
@@ -395,17 +519,13 @@ static int upload(ipdg_ctx c, Tp** dst, const Tp* src, size_t n) {
   if (n) CUDA_TRY(c, cudaMemcpy(*dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice));
   return IPDG_OK;
 }
-#define TRY(x)                 \
-  do {                         \
-    int rc_ = (x);             \
-    if (rc_ != IPDG_OK) return rc_; \
-  } while (0)
 
 static void free_mesh(ipdg_ctx c) {
-  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy};
+  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->geo = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
+  c->nbg = nullptr; c->W2 = nullptr;
   c->bcode = nullptr;
   c->vxy = nullptr;
   for (auto& g : c->gexec)
@@ -663,6 +783,15 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   TRY(upload(c, &c->bcode, bcv.data(), bcv.size()));
   c->etoe_h = etoe;
   c->etof_h = etof;
+  {  // split variant: neighbour element ids (self on boundary faces) + the same face codes
+    std::vector<int4> nbg(K);
+    for (int64_t e = 0; e < K; ++e) {
+      int id[3];
+      for (int f = 0; f < 3; ++f) id[f] = etoe[e * 3 + f] >= 0 ? etoe[e * 3 + f] : (int)e;
+      nbg[e] = make_int4(id[0], id[1], id[2], (int)(unsigned short)nbr[e].w);
+    }
+    TRY(upload(c, &c->nbg, nbg.data(), nbg.size()));
+  }
   const int64_t KH = K + H;
   CUDA_TRY(c, cudaMalloc(&c->geo, KH * sizeof(double4)));
   unsigned long long* bad = nullptr;
@@ -1207,5 +1336,14 @@ int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
 }
 
 int64_t ipdg_launch_count(ipdg_ctx c) { return c ? c->launches : -1; }
+
+int ipdg_set_variant(ipdg_ctx c, int variant) {
+  if (!c || variant < 0 || variant > 2) return IPDG_EINVAL;
+  c->variant = variant;
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->gkey_x = nullptr;
+  return IPDG_OK;
+}
 
 }  // extern "C"

@@ -20,11 +20,14 @@ def _mesh():
 
 @pytest.mark.parametrize("N", [1, 4, 6, 8])
 @pytest.mark.parametrize("P", [2, 3])
-def test_partitioned_ax_loopback(N, P):
+@pytest.mark.parametrize("variant", [1, 2])
+def test_partitioned_ax_loopback(N, P, variant):
     m = _mesh()
     part = meshgen.rcb_partition(m["VX"], m["VY"], m["EToV"], P)
     ranks = partition.split(m, part, P)
     ops = [Ipdg.from_rank_mesh(N, rm) for rm in ranks]
+    for op in ops:
+        op.set_variant(variant)
     Np = ops[0].Np
     u = meshgen.uniform_field(m["EToV"].shape[0], Np, 100 + N)
     uloc = [torch.from_numpy(u[rm.elems]).cuda() for rm in ranks]
@@ -39,7 +42,9 @@ def test_partitioned_ax_loopback(N, P):
     Au = np.zeros_like(u)
     for rm, op, ul in zip(ranks, ops, uloc):
         Au[rm.elems] = op.ax(ul).cpu().numpy()
-    ref = Ipdg(N, m).ax(torch.from_numpy(u).cuda()).cpu().numpy()
+    gop = Ipdg(N, m)
+    gop.set_variant(variant)
+    ref = gop.ax(torch.from_numpy(u).cuda()).cpu().numpy()
     assert np.abs(Au - ref).max() <= 1e-14 * np.abs(ref).max()
     A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], RefElem(N))
     Ao = A @ u.ravel()

@@ -151,3 +151,18 @@ def test_full_size_c2_parity(N):
     # element-wise too: worst element relative to its own scale
     err = np.abs(Au - Ao).max(axis=1) / np.maximum(np.abs(Ao).max(axis=1), 1e-300)
     assert err.max() <= 1e-11
+
+
+@pytest.mark.parametrize("N", range(1, 9))
+@pytest.mark.parametrize("variant", [1, 2])
+def test_ax_kernel_variants(N, variant):
+    """Fused k_sipdg (variant 1) and split k_grad + k_flux (variant 2) both match the oracle."""
+    m = MESHES["mixed_bc"]()
+    ref = RefElem(N)
+    op = Ipdg(N, m)
+    op.set_variant(variant)
+    for lam in (0.0, 0.5):
+        A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+        u = meshgen.uniform_field(op.K, op.Np, seed=200 + N)
+        Au = op.ax(gpu(u), lam=lam).cpu().numpy()
+        assert rel(Au.ravel(), A @ u.ravel()) <= TOL, (N, variant, lam)

@@ -16,11 +16,12 @@ def gpu(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def check_solve(m, N, precond, tol, lam=0.0, maxit=20000, f=meshgen.sin_sin_forcing):
+def check_solve(m, N, precond, tol, lam=0.0, maxit=20000, f=meshgen.sin_sin_forcing, variant=0):
     ref = RefElem(N)
     A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
     b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, f)
     op = Ipdg(N, m)
+    op.set_variant(variant)
     x, st = op.pcg_solve(gpu(b), lam=lam, precond=precond, tol=tol, maxit=maxit)
     dinv = 1.0 / A.diagonal() if precond else None
     xo, sto = solvers.pcg(lambda v: A @ v, b.ravel(), tol, maxit, dinv=dinv)
@@ -65,6 +66,12 @@ def test_jacobi_nearly_neumann_long_solve(N):
     assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
     r = b.ravel() - A @ x.cpu().numpy().ravel()
     assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b) * 1.05
+
+
+@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1)])
+def test_pcg_other_kernel_variant(N, variant):
+    m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=13)
+    check_solve(m, N, 1, 1e-9, variant=variant)
 
 
 def test_screened_poisson_lambda():
