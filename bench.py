@@ -393,8 +393,9 @@ def run_sweep(args):
     nx = args.sweep_nx
     mesh = meshgen.square(nx, jitter=0.2, diag="random", order="morton", seed=3)
     stream = torch.cuda.current_stream()
-    for N in range(1, 9):
+    for N, variant in [(N, v) for N in range(1, 9) for v in args.sweep_variants]:
         op = Ipdg(N, mesh)
+        op.set_variant(variant)
         K, Np = op.K, op.Np
         nbuf = max(2, int(math.ceil(4 * 126e6 / (2 * 8 * K * Np))))
         us = [torch.rand(K, Np, dtype=torch.float64, device="cuda") for _ in range(nbuf)]
@@ -413,7 +414,7 @@ def run_sweep(args):
         bmin = (16 * Np + 48) * K
         fmin = ax_flops_per_elem(N) * K
         t_roof = max(bmin / (pk["hbm_gbs"] * 1e9), fmin / (FP64_PEAK_TFLOPS * 1e12))
-        print(json.dumps({"sweep": "C3", "N": N, "K": K, "dofs": K * Np, "ms": round(ms, 5),
+        print(json.dumps({"sweep": "C3", "N": N, "variant": variant, "K": K, "dofs": K * Np, "ms": round(ms, 5),
                           "gdofs": round(K * Np / (ms / 1e3) / 1e9, 3),
                           "hbm_gbs_algorithmic": round(bmin / (ms / 1e3) / 1e9, 1),
                           "hbm_frac": round(bmin / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
@@ -439,6 +440,7 @@ def main():
     ap.add_argument("--ref-nx", type=int, default=50)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-nx", type=int, default=707)
+    ap.add_argument("--sweep-variants", type=int, nargs="+", default=[0], help="0 auto, 1 fused, 2 split")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

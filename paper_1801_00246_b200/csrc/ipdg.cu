@@ -321,7 +321,8 @@ struct Impl {
     return IPDG_OK;
   }
 
-  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
+  // auto: the faster variant measured per degree on C3 (profiles/r01_sweep_variants.jsonl)
+  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && !(N == 2 || N == 4 || N == 5)); }
 
   static SplitArgs sargs(ipdg_ctx c) {
     SplitArgs a;

@@ -13,9 +13,11 @@ ap.add_argument("--N", type=int, default=4)
 ap.add_argument("--nx", type=int, default=316)
 ap.add_argument("--ax", type=int, default=3)
 ap.add_argument("--pcg", type=int, default=3)
+ap.add_argument("--variant", type=int, default=0)
 a = ap.parse_args()
 mesh = meshgen.square(a.nx, jitter=0.2, diag="random", order="morton", seed=2)
 op = Ipdg(a.N, mesh)
+op.set_variant(a.variant)
 u = torch.rand(op.K, op.Np, dtype=torch.float64, device="cuda")
 for _ in range(a.ax):
     op.ax(u)
