@@ -435,7 +435,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=200)
+    ap.add_argument("--cpu-iters", type=int, default=600)
     ap.add_argument("--cpu-nx", type=int, default=100)
     ap.add_argument("--ref-nx", type=int, default=50)
     ap.add_argument("--sweep", action="store_true")
