@@ -148,8 +148,9 @@ def build_mesh(world, rank):
 
 
 def pass_a_bytes_per_elem(Np, precond):
-    # reads r, dinv, p_{k-1}, x; writes p_k, x, Ap (8 B each per DOF) + 4 geometric doubles + 8 B neighbour slots
-    vec = (7 if precond else 6) * 8 * Np
+    # reads z = D^-1 r (written by pass B), p_{k-1}, x; writes p_k, x, Ap (8 B each per DOF)
+    # + 4 geometric doubles + 8 B neighbour slots.  (Pass B: reads r, Ap, D^-1; writes r, z.)
+    vec = 6 * 8 * Np
     return vec + 32 + 8
 
 

@@ -74,7 +74,7 @@ struct ipdg_ctx_s {
   void* ws = nullptr;
   int64_t ws_bytes = 0;
   bool ws_owned = false;
-  double *r = nullptr, *pe = nullptr, *po = nullptr, *Ap = nullptr, *dinv = nullptr;
+  double *r = nullptr, *pe = nullptr, *po = nullptr, *Ap = nullptr, *dinv = nullptr, *zb = nullptr;
   double dinv_lambda = -1.0;
   bool dinv_valid = false;
   // current solve
@@ -365,8 +365,7 @@ struct Impl {
     SplitArgs a = sargs(c);
     a.W2 = c->W2;
     a.lambda = c->lambda;
-    a.r = c->r;
-    a.dinv = c->precond ? c->dinv : nullptr;
+    a.z = c->precond ? c->zb : c->r;
     a.p_even = c->pe;
     a.p_odd = c->po;
     a.x = c->x;
@@ -420,6 +419,7 @@ struct Impl {
     a.lambda = c->lambda;
     a.r = c->r;
     a.dinv = c->precond ? c->dinv : nullptr;
+    a.z = c->precond ? c->zb : c->r;
     a.p_even = c->pe;
     a.p_odd = c->po;
     a.x = c->x;
@@ -498,7 +498,7 @@ static int ghost_cap_n(int device) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (optin <= 0) optin = 227 * 1024;
   const int fixed = SmemLayout::make<N>(0, true, true).total * 8 + 1024;  // + static smem
-  const int per = (T::SU + T::SG + 2 + std::max(T::SXY, 3 * T::NP)) * 8;
+  const int per = (T::SU + T::SG + 2 + std::max(T::SXY, 2 * T::NP)) * 8;  // slot + ids (+ PCG staging aliasing w)
   int g = (optin - fixed) / per;
   g = g / 8 * 8;
   return std::max(8, std::min(g, 30000 - T::E));
@@ -545,7 +545,7 @@ static void free_ws(ipdg_ctx c) {
   c->ws = nullptr;
   c->ws_owned = false;
   c->ws_bytes = 0;
-  c->r = c->pe = c->po = c->Ap = c->dinv = nullptr;
+  c->r = c->pe = c->po = c->Ap = c->dinv = c->zb = nullptr;
   c->dinv_valid = false;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
@@ -872,9 +872,8 @@ __global__ void k_pack_rows(int64_t S, int NP, const int* __restrict__ idx, cons
 }
 
 // p_k = D^-1 r + beta p_{k-1} at the send rows, with the same decisions as pass A's prologue
-__global__ void k_pack_p(int64_t S, int NP, const int* __restrict__ idx, const double* __restrict__ r,
-                         const double* __restrict__ dinv, const double* p_even, const double* p_odd,
-                         const PcgState* st, double* __restrict__ out) {
+__global__ void k_pack_p(int64_t S, int NP, const int* __restrict__ idx, const double* __restrict__ z,
+                         const double* p_even, const double* p_odd, const PcgState* st, double* __restrict__ out) {
   if (st->stop_iter >= 0) return;
   const long long k = st->it + 1;
   const bool first = (k == 1);
@@ -885,8 +884,7 @@ __global__ void k_pack_p(int64_t S, int NP, const int* __restrict__ idx, const d
   const int64_t s = t / NP;
   const int i = (int)(t - s * NP);
   const int64_t g = (int64_t)idx[s] * NP + i;
-  const double z = dinv ? r[g] * dinv[g] : r[g];
-  out[t] = first ? z : z + beta * pold[g];
+  out[t] = first ? z[g] : z[g] + beta * pold[g];
 }
 
 static int halo_exchange(ipdg_ctx c, cudaStream_t s) {
@@ -974,7 +972,7 @@ int ipdg_workspace_bytes(ipdg_ctx c, int64_t* bytes) {
   if (!c || !bytes) return IPDG_EINVAL;
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "workspace size needs a mesh");
   const int64_t n = (c->K + c->H) * c->ref.Np;
-  *bytes = 5 * ((n * 8 + 255) / 256 * 256);
+  *bytes = 6 * ((n * 8 + 255) / 256 * 256);
   return IPDG_OK;
 }
 
@@ -987,6 +985,7 @@ static int bind_ws(ipdg_ctx c) {
   c->po = (double*)(b + 2 * seg);
   c->Ap = (double*)(b + 3 * seg);
   c->dinv = (double*)(b + 4 * seg);
+  c->zb = (double*)(b + 5 * seg);
   c->dinv_valid = false;
   return IPDG_OK;
 }
@@ -1037,8 +1036,8 @@ static int halo_for_p(ipdg_ctx c, cudaStream_t s) {
   if (!c->comm) FAIL(c, IPDG_ESTATE, "distributed PCG needs a communicator (ipdg_comm_init)");
   const int64_t n = c->S * c->ref.Np;
   if (n) {
-    k_pack_p<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, c->r,
-                                                         c->precond ? c->dinv : nullptr, c->pe, c->po, c->st, c->sendbuf);
+    k_pack_p<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, c->precond ? c->zb : c->r,
+                                                         c->pe, c->po, c->st, c->sendbuf);
     c->launches++;
   }
   return halo_exchange(c, s);
@@ -1048,8 +1047,8 @@ static int one_iteration(ipdg_ctx c, cudaStream_t s) {
   TRY(halo_for_p(c, s));
   TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
   TRY(allreduce(c, &c->st->red_A, 1, s));
-  k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->st,
-                                        c->partials, c->counter);
+  k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
+                                        c->st, c->partials, c->counter);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   TRY(allreduce(c, c->st->red_B, 2, s));
@@ -1101,7 +1100,8 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   *c->st_host = h;
   CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
   TRY(ipdg_ax(c, x, c->Ap, lambda, stream));
-  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->st, c->partials, c->counter);
+  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->zb, c->st, c->partials,
+                                         c->counter);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   TRY(allreduce(c, c->st->red_B, 3, s));
@@ -1158,8 +1158,8 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b,
       if (rc != IPDG_OK) break;
       if ((rc = allreduce(c, &c->st->red_A, 1, s)) != IPDG_OK) break;
       cudaEventRecord(ev[3 * i + 1], s);
-      k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->st,
-                                            c->partials, c->counter);
+      k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
+                                            c->st, c->partials, c->counter);
       c->launches++;
       cudaEventRecord(ev[3 * i + 2], s);
       if ((rc = allreduce(c, c->st->red_B, 2, s)) != IPDG_OK) break;

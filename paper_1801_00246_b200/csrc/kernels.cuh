@@ -85,6 +85,7 @@ struct AxArgs {
   // MODE_PCG_A
   const double* r;
   const double* dinv;    // null: no preconditioner
+  const double* z;       // z = D^-1 r (written by pass B / init), = r without preconditioner
   double* p_even;        // p_k lives in p_even when k is even, p_odd when k is odd
   double* p_odd;         //   (double buffer: ghosts read p_{k-1} while owners write p_k)
   double* x;             // deferred update x += alpha_{k-1} p_{k-1}

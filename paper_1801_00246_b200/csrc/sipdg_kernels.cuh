@@ -68,7 +68,7 @@ struct SmemLayout {
     // PCG staging of r, D^-1, p_{k-1}, x (own) and r, D^-1, p_{k-1} (ghosts) aliases uxy / fa,
     // which are produced only after the staging has been consumed
     L.stg = L.uxy;
-    const int need = pcg ? (4 * T::E + 3 * gm8) * T::NP : 0;
+    const int need = pcg ? (3 * T::E + 2 * gm8) * T::NP : 0;
     if (L.stg + need > o) o = L.stg + need;
     L.total = o;
     return L;
@@ -277,29 +277,24 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
         cp_async8(us + (E + g) * SU + i, srcp + i);
       });
     } else {
-      double* sr = stg;                  // own: r | dinv | p_{k-1} | x, then ghosts: r | dinv | p_{k-1}
-      double* sd = stg + E * NP;
-      double* sp = stg + 2 * E * NP;
-      double* sx = stg + 3 * E * NP;
-      double* gr = stg + 4 * E * NP;
-      double* gd = gr + gm8 * NP;
-      double* gp = gd + gm8 * NP;
-      const double* dv = a.dinv;
+      double* sz = stg;                  // own: z | p_{k-1} | x, then ghosts: z | p_{k-1}
+      double* sp = stg + E * NP;
+      double* sx = stg + 2 * E * NP;
+      double* gz = stg + 3 * E * NP;
+      double* gp = gz + gm8 * NP;
       for_rows<N>(Eb, warp, lane, [&](int e, int i) {
         const int64_t g = (e0 + e) * NP + i;
-        cp_async8(sr + e * NP + i, a.r + g);
-        if (dv) cp_async8(sd + e * NP + i, dv + g);
+        cp_async8(sz + e * NP + i, a.z + g);
         if (!first) cp_async8(sp + e * NP + i, pold + g);
         if (do_xupd) cp_async8(sx + e * NP + i, a.x + g);
       });
       for_rows<N>(Gb, warp, lane, [&](int q, int i) {
         const int ge = gids[q];
         if (ge >= K) {
-          cp_async8(gr + q * NP + i, a.halo_p + (int64_t)(ge - K) * NP + i);
+          cp_async8(gz + q * NP + i, a.halo_p + (int64_t)(ge - K) * NP + i);
         } else {
           const int64_t g = (int64_t)ge * NP + i;
-          cp_async8(gr + q * NP + i, a.r + g);
-          if (dv) cp_async8(gd + q * NP + i, dv + g);
+          cp_async8(gz + q * NP + i, a.z + g);
           if (!first) cp_async8(gp + q * NP + i, pold + g);  // p_{k-1}; owners write p_k elsewhere
         }
       });
@@ -322,19 +317,16 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     }
     cp_async_wait_group1();  // this block's data complete; the prefetch may still fly
     __syncthreads();
-    if (MODE == MODE_PCG_A) {  // p_k = D^-1 r + beta p_{k-1} (own + ghosts); x += alpha_{k-1} p_{k-1}
-      const double* sr = stg;
-      const double* sd = stg + E * NP;
-      const double* sp = stg + 2 * E * NP;
-      const double* sx = stg + 3 * E * NP;
-      const double* gr = stg + 4 * E * NP;
-      const double* gd = gr + gm8 * NP;
-      const double* gp = gd + gm8 * NP;
-      const bool pre = a.dinv != nullptr;
+    if (MODE == MODE_PCG_A) {  // p_k = z + beta p_{k-1} (own + ghosts); x += alpha_{k-1} p_{k-1}
+      const double* sz = stg;
+      const double* sp = stg + E * NP;
+      const double* sx = stg + 2 * E * NP;
+      const double* gz = stg + 3 * E * NP;
+      const double* gp = gz + gm8 * NP;
       for_rows<N>(Eb, warp, lane, [&](int e, int i) {
         const int o = e * NP + i;
         const double po = first ? 0.0 : sp[o];
-        const double v = (pre ? sr[o] * sd[o] : sr[o]) + beta * po;
+        const double v = sz[o] + beta * po;
         const int64_t g = (e0 + e) * NP + i;
         pnew[g] = v;
         if (do_xupd) a.x[g] = sx[o] + alpha_prev * po;
@@ -342,9 +334,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
       });
       for_rows<N>(Gb, warp, lane, [&](int q, int i) {
         const int o = q * NP + i;
-        double v;
-        if (gids[q] >= K) v = gr[o];
-        else v = (pre ? gr[o] * gd[o] : gr[o]) + (first ? 0.0 : beta * gp[o]);
+        const double v = (gids[q] >= K || first) ? gz[o] : gz[o] + beta * gp[o];
         us[(E + q) * SU + i] = v;
       });
       __syncthreads();
@@ -526,8 +516,8 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
 
 // ---- PCG pass B: r -= alpha A p; z = D^{-1} r; partial (r.z, r.r)
 __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r, const double* __restrict__ Ap,
-                                               const double* __restrict__ dinv, PcgState* st, double* partials,
-                                               unsigned int* counter) {
+                                               const double* __restrict__ dinv, double* __restrict__ z, PcgState* st,
+                                               double* partials, unsigned int* counter) {
   __shared__ double red[32 * 3];
   if (st->stop_iter >= 0) return;
   const long long k = st->it + 1;
@@ -549,6 +539,7 @@ __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r
     const double ri = r[i] - alpha * Ap[i];
     r[i] = ri;
     const double zi = dinv ? ri * dinv[i] : ri;
+    if (dinv) z[i] = zi;
     rz += ri * zi;
     rr += ri * ri;
   }
@@ -562,8 +553,9 @@ __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r
 
 // ---- PCG start: r = b - A x0, partial (r.z, r.r, b.b)
 __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
-                                                  double* __restrict__ r, const double* __restrict__ dinv, PcgState* st,
-                                                  double* partials, unsigned int* counter) {
+                                                  double* __restrict__ r, const double* __restrict__ dinv,
+                                                  double* __restrict__ z, PcgState* st, double* partials,
+                                                  unsigned int* counter) {
   __shared__ double red[32 * 3];
   double rz = 0.0, rr = 0.0, bb = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -571,6 +563,7 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const double* __res
     const double ri = bi - Ax[i];
     r[i] = ri;
     const double zi = dinv ? ri * dinv[i] : ri;
+    if (dinv) z[i] = zi;
     rz += ri * zi;
     rr += ri * ri;
     bb += bi * bi;

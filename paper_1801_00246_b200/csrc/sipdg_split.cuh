@@ -27,8 +27,7 @@ struct SplitArgs {
   const double* halo;    // [H] ghost rows (AX: u, PCG: p_k)
   double* W2;            // [(K+H) x 2 Np]
   double* Au;
-  const double* r;
-  const double* dinv;
+  const double* z;       // D^-1 r (or r)
   double* p_even;
   double* p_odd;
   double* x;
@@ -123,9 +122,8 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
         v = __ldg(a.u + e * NP + i);
       } else {
         const int64_t g = e * NP + i;
-        const double z = a.dinv ? __ldg(a.r + g) * __ldg(a.dinv + g) : __ldg(a.r + g);
         const double po = d.first ? 0.0 : pold[g];
-        v = z + d.beta * po;
+        v = __ldg(a.z + g) + d.beta * po;
         pnew[g] = v;
         if (d.do_xupd) a.x[g] += d.alpha_prev * po;
       }
