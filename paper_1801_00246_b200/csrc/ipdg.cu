@@ -1338,6 +1338,21 @@ int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
 
 int64_t ipdg_launch_count(ipdg_ctx c) { return c ? c->launches : -1; }
 
+// debug (not in ipdg.h): per-phase cycle counters of k_sipdg when built with -DIPDG_PHASE_TIMING
+int ipdg_debug_phase_cycles(unsigned long long* out8, int reset) {
+  if (!out8) return IPDG_EINVAL;
+#ifdef IPDG_PHASE_TIMING
+  if (cudaMemcpyFromSymbol(out8, ipdg_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess) return IPDG_ECUDA;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(ipdg_phase_cycles, z, sizeof(z)) != cudaSuccess) return IPDG_ECUDA;
+  }
+#else
+  for (int i = 0; i < 8; ++i) out8[i] = 0;
+#endif
+  return IPDG_OK;
+}
+
 int ipdg_set_variant(ipdg_ctx c, int variant) {
   if (!c || variant < 0 || variant > 2) return IPDG_EINVAL;
   c->variant = variant;

@@ -19,7 +19,7 @@
 namespace ipdg {
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -40,6 +40,22 @@ __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 enum { MODE_AX = 0, MODE_PCG_A = 1 };
+
+// Optional phase timing (compile with -DIPDG_PHASE_TIMING; tools/phase_timing.py): warp 0 of every
+// CTA accumulates clock64() deltas per phase into ipdg_phase_cycles[8].
+#ifdef IPDG_PHASE_TIMING
+__device__ unsigned long long ipdg_phase_cycles[8];
+#define PHASE_MARK(id)                                                   \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long t_ = clock64();                                    \
+      atomicAdd(&ipdg_phase_cycles[id], (unsigned long long)(t_ - ph_t)); \
+      ph_t = t_;                                                         \
+    }                                                                    \
+  } while (0)
+#else
+#define PHASE_MARK(id) do { } while (0)
+#endif
 
 // shared-memory layout (in doubles) shared by host and device
 struct SmemLayout {
@@ -247,6 +263,9 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
   }
   double wr[NT][2], ws[NT][2];
   int par = 0;
+#ifdef IPDG_PHASE_TIMING
+  long long ph_t = clock64();
+#endif
   int cur_e0 = 0, cur_Eb = 0, cur_Gb = 0;  // block metadata, prefetched one block ahead
   if (blockIdx.x < a.nblocks) {
     cur_e0 = a.boff[blockIdx.x];
@@ -261,6 +280,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     int* gids = gids0 + par * gm8;
     cp_async_wait_all();
     __syncthreads();  // previous block done with the buffers; this block's gids / nbr landed
+    PHASE_MARK(0);  // wait for the previous block's stragglers + this block's metadata
     // ---- P0: async copies of the element data of this block
     for (int q = tid; q < 2 * (Eb + Gb); q += NTHR) {  // raw geometry r_x s_x r_y s_y (2 x 16 B)
       const int s = q >> 1, h = q & 1;
@@ -340,6 +360,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
       __syncthreads();
     }
 
+    PHASE_MARK(1);  // P0: loads (and PCG prep)
     // ---- P1: reference gradient on DMMA; u_x, u_y to smem; w_r / w_s kept for own tiles
     const int ntiles = W + (Gb + 7) / 8;
     for (int t = warp; t < ntiles; t += W) {
@@ -402,6 +423,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     }
     __syncthreads();
 
+    PHASE_MARK(2);  // P1 incl. the barrier
     // ---- P2 + P3 per warp on its own tile (no block barrier in between)
     if (8 * warp < Eb) {
       // P2: four lanes per element, one face node per lane and pass: jumps and fluxes, kept in
@@ -445,6 +467,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
           }
         }
       }
+      PHASE_MARK(3);  // P2 (warp 0)
       // P3: Au = [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss; E^T] (+ lambda J u M)
       const int e = 8 * warp + (lane >> 2);
       double C[NT][2];
@@ -487,6 +510,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
           for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
         }
       }
+      PHASE_MARK(4);  // P3 GEMM (warp 0)
       if (e < Eb) {
         const int64_t base = (e0 + e) * NP;
 #pragma unroll
@@ -500,6 +524,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
             }
           }
       }
+      PHASE_MARK(5);  // P3 stores (warp 0)
     }
   }
   cp_async_wait_all();
