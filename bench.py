@@ -136,15 +136,32 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------- workload
-def build_mesh(world, rank):
+CONFIGS = {
+    # BASELINE.json configs[1]: single-B200 Ax throughput, N=4, ~200k-triangle unstructured square
+    "C2": dict(N=4, desc="jittered %dx%d-cell unit square (Morton order, all Dirichlet)" % (C2["nx"], C2["nx"])),
+    # configs[3]: Jacobi-PCG pressure Poisson at N=6 on a channel-with-cylinder mesh (~2M triangles), strong scaling
+    "C4": dict(N=6, desc="channel [-16,25]x[-22,22] minus the unit square cylinder, graded, 1.84M triangles "
+                        "(outflow Dirichlet, other boundaries Neumann)"),
+    # configs[4]: weak scaling at N=8, 4M triangles per GPU
+    "C5": dict(N=8, desc="one 1414x1414-cell tile (3,998,792 triangles) per GPU, all Dirichlet"),
+}
+
+
+def build_mesh(config, world, rank):
+    """Global mesh and element -> rank map (None on one GPU)."""
     from paper_1801_00246_b200 import meshgen
-    if world == 1:
-        m = meshgen.square(C2["nx"], jitter=C2["jitter"], diag=C2["diag"], order=C2["order"], seed=C2["seed"])
-        return m, None
-    px = {2: 2, 4: 2, 8: 4}.get(world, world)
-    py = world // px
-    mesh, part = meshgen.tiles(C2["nx"], px, py, jitter=C2["jitter"], seed=C2["seed"])
-    return mesh, part
+    if config == "C4":
+        m = meshgen.cylinder()
+        part = None if world == 1 else meshgen.rcb_partition(m["VX"], m["VY"], m["EToV"], world)
+        return m, part
+    if config == "C5" or world > 1:
+        n = 1414 if config == "C5" else C2["nx"]
+        px = {1: 1, 2: 2, 4: 2, 8: 4}.get(world, world)
+        py = world // px
+        mesh, part = meshgen.tiles(n, px, py, jitter=C2["jitter"], seed=C2["seed"])
+        return mesh, (part if world > 1 else None)
+    m = meshgen.square(C2["nx"], jitter=C2["jitter"], diag=C2["diag"], order=C2["order"], seed=C2["seed"])
+    return m, None
 
 
 def pass_a_bytes_per_elem(Np, precond):
@@ -208,20 +225,24 @@ def _solve(op, b, xs, stream, world, dev):
     barrier(world)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
-    _, sst = op.pcg_solve(b, xs, precond=1, tol=1e-8, maxit=100000)
+    _, sst = op.pcg_solve(b, xs, precond=1, tol=1e-8, maxit=_solve.maxit)
     s1.record(stream)
     torch.cuda.synchronize()
     return max_over_ranks(s0.elapsed_time(s1), world, dev), sst
 
 
+_solve.maxit = 100000
+
+
 def run_ours(args):
+    _solve.maxit = args.maxit
     import torch
     from paper_1801_00246_b200 import Ipdg, meshgen
     world, rank, local = dist_setup("nccl")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    N = C2["N"]
-    mesh, part = build_mesh(world, rank)
+    N = CONFIGS[args.config]["N"]
+    mesh, part = build_mesh(args.config, world, rank)
     if world > 1:
         op = Ipdg.distributed(N, mesh, part, rank, world, device=local)
     else:
@@ -229,7 +250,12 @@ def run_ours(args):
     K, Np = op.K, op.Np
     # right-hand side b = J M f_I of the manufactured problem (setup, not timed)
     x_nodes, y_nodes = op.nodes()
-    f = 2 * math.pi ** 2 * torch.sin(math.pi * x_nodes) * torch.sin(math.pi * y_nodes)  # -Lap of sin sin
+    if args.config == "C4":  # f = exp(-((x-2)^2 + y^2)/4)
+        f = torch.exp(-((x_nodes - 2.0) ** 2 + y_nodes ** 2) / 4.0)
+    else:  # -Lap of sin(pi x / Px) sin(pi y / Py) on the (tiled) domain; Px = Py = 1 on one GPU
+        Px = float(mesh["VX"].max() - mesh["VX"].min())
+        Py = float(mesh["VY"].max() - mesh["VY"].min())
+        f = math.pi ** 2 * (1 / Px ** 2 + 1 / Py ** 2) * torch.sin(math.pi * x_nodes / Px) * torch.sin(math.pi * y_nodes / Py)
     b = op.mass(f)
     x = torch.zeros_like(b)
     stream = torch.cuda.current_stream()
@@ -314,9 +340,9 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 6), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: Jacobi-PCG iteration (pass A: p-update + SIPDG Ax + p.Ap; pass B: r-update + r.z, r.r) "
-                               "on a jittered %dx%d-cell unit square, %d triangles per GPU, N=%d, Morton order, "
-                               "all-Dirichlet, manufactured sin(pi x) sin(pi y) RHS" % (C2["nx"], C2["nx"], K, N),
+        "config": {"workload": "%s: Jacobi-PCG iteration (pass A: p-update + SIPDG Ax + p.Ap; pass B: r-update + r.z, r.r) "
+                               "on a %s; %d triangles on this rank, N=%d, manufactured right-hand side"
+                               % (args.config, CONFIGS[args.config]["desc"], K, N),
                    "N": N, "K_per_gpu": K, "dofs_total": int(dofs_total), "precond": "jacobi",
                    "l2": "working set 6 x K x Np x 8 B = %.0f MB > 126 MB L2 (no flush needed)" % (6 * 8 * K * Np / 1e6),
                    "parallelism": "element partition, %d rank(s)" % world},
@@ -436,6 +462,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--maxit", type=int, default=100000, help="iteration cap of the timed full solve")
     ap.add_argument("--cpu-iters", type=int, default=600)
     ap.add_argument("--cpu-nx", type=int, default=100)
     ap.add_argument("--ref-nx", type=int, default=50)
