@@ -426,11 +426,29 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     PHASE_MARK(2);  // P1 incl. the barrier
     // ---- P2 + P3 per warp on its own tile (no block barrier in between)
     if (8 * warp < Eb) {
-      // P2: four lanes per element, one face node per lane and pass: jumps and fluxes, kept in
-      // registers exactly where the face block's A fragments need them (A[e = lane>>2][k = lane&3])
-      double far[T::NQ], fas[T::NQ], fag[T::NQ];
+      // P3 starts with the volume part, Au = [w_r | w_s] x [Sr; Ss], straight from registers;
+      // P2 then produces the face block one face-node pass at a time (four lanes per element, the
+      // values land exactly where the A fragments need them: A[e = lane>>2][k = lane&3]) and each
+      // pass is fed to the tensor cores at once, so the scalar face work overlaps the DMMAs.
+      const int e = 8 * warp + (lane >> 2);
+      double C[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) C[nt][0] = C[nt][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < 2 * NT; ++c) {
+        const double av = wr[c >> 1][c & 1];
+        const double* bt = tabM + c * NT * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2 * NT; ++c) {
+        const double av = ws[c >> 1][c & 1];
+        const double* bt = tabM + (2 * NT + c) * NT * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
+      }
       {
-        const int e = 8 * warp + (lane >> 2);
         const int ec = e < Eb ? e : 8 * warp;  // rows past the block end compute on a valid slot, never stored
         const short4 nb = nbs[ec];
         const double* uo = us + ec * SU;
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
         const double* fq0 = fgs + ec;
 #pragma unroll
         for (int q = 0; q < T::NQ; ++q) {
-          far[q] = fas[q] = fag[q] = 0.0;
+          double far = 0.0, fas = 0.0, fag = 0.0;
           const int it = itab[q];
           if (it >= 0) {
             const int f = it >> 24, kk = (it >> 16) & 255, i = it & 65535;
@@ -461,44 +479,22 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
             const double tp = (pf == 0) ? -wsn : (pf == 1) ? wrn + wsn : -wrn;
             const double tq = (bc == 1) ? tp : -tp;                 // sJ n-.grad u+ after mirroring
             const double delta = ((bc == 1) ? -upr : upr) - um;     // paper jump
-            far[q] = fq[0] * delta;                                 // 1/2 sJ (n.grad r) delta
-            fas[q] = fq[T::FGS] * delta;                            // 1/2 sJ (n.grad s) delta
-            fag[q] = -0.5 * (tm + tq) - fq[2 * T::FGS] * delta;     // -sJ (n.{grad u} + tau delta)
+            far = fq[0] * delta;                                    // 1/2 sJ (n.grad r) delta
+            fas = fq[T::FGS] * delta;                               // 1/2 sJ (n.grad s) delta
+            fag = -0.5 * (tm + tq) - fq[2 * T::FGS] * delta;        // -sJ (n.{grad u} + tau delta)
+          }
+          const double* b0 = tabM + (KCW + q) * NT * 32 + lane;
+          const double* b1 = tabM + (KCW + T::NQ + q) * NT * 32 + lane;
+          const double* b2 = tabM + (KCW + 2 * T::NQ + q) * NT * 32 + lane;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma(C[j][0], C[j][1], far, b0[j * 32]);
+            dmma(C[j][0], C[j][1], fas, b1[j * 32]);
+            dmma(C[j][0], C[j][1], fag, b2[j * 32]);
           }
         }
       }
-      PHASE_MARK(3);  // P2 (warp 0)
-      // P3: Au = [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss; E^T] (+ lambda J u M)
-      const int e = 8 * warp + (lane >> 2);
-      double C[NT][2];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) C[nt][0] = C[nt][1] = 0.0;
-#pragma unroll
-      for (int c = 0; c < 2 * NT; ++c) {
-        const double av = wr[c >> 1][c & 1];
-        const double* bt = tabM + c * NT * 32 + lane;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
-      }
-#pragma unroll
-      for (int c = 0; c < 2 * NT; ++c) {
-        const double av = ws[c >> 1][c & 1];
-        const double* bt = tabM + (2 * NT + c) * NT * 32 + lane;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], av, bt[j * 32]);
-      }
-#pragma unroll
-      for (int q = 0; q < T::NQ; ++q) {
-        const double* b0 = tabM + (KCW + q) * NT * 32 + lane;
-        const double* b1 = tabM + (KCW + T::NQ + q) * NT * 32 + lane;
-        const double* b2 = tabM + (KCW + 2 * T::NQ + q) * NT * 32 + lane;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          dmma(C[j][0], C[j][1], far[q], b0[j * 32]);
-          dmma(C[j][0], C[j][1], fas[q], b1[j * 32]);
-          dmma(C[j][0], C[j][1], fag[q], b2[j * 32]);
-        }
-      }
+      PHASE_MARK(3);  // P2 + P3 GEMM (warp 0)
       if (LAM) {
         const double lj = a.lambda * geos[e * SG + 4];
         const double* urow = us + e * SU + (lane & 3);
