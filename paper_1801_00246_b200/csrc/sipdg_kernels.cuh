@@ -39,6 +39,24 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 enum { MODE_AX = 0, MODE_PCG_A = 1 };
 
 // Optional phase timing (compile with -DIPDG_PHASE_TIMING; tools/phase_timing.py): warp 0 of every
@@ -59,7 +77,7 @@ __device__ unsigned long long ipdg_phase_cycles[8];
 
 // shared-memory layout (in doubles) shared by host and device
 struct SmemLayout {
-  int tabG, tabM, tabL, iaux, us, geo, fg, nb, gid, uxy, fa, stg, total;  // offsets in doubles
+  int tabG, tabM, tabL, iaux, us, geo, fg, nb, gid, uxy, fa, stg, mbar, total;  // offsets in doubles
   template <int N>
   __host__ __device__ static SmemLayout make(int gmax, bool lam, bool pcg) {
     using T = Tr<N>;
@@ -84,8 +102,9 @@ struct SmemLayout {
     // PCG staging of r, D^-1, p_{k-1}, x (own) and r, D^-1, p_{k-1} (ghosts) aliases uxy / fa,
     // which are produced only after the staging has been consumed
     L.stg = L.uxy;
-    const int need = pcg ? (3 * T::E + 2 * gm8) * T::NP : 0;
+    const int need = pcg ? 3 * (T::E * T::NP + 2) + 2 * gm8 * T::NP : 0;  // own arrays padded for TMA alignment
     if (L.stg + need > o) o = L.stg + need;
+    L.mbar = o; o += 1;
     L.total = o;
     return L;
   }
@@ -185,6 +204,9 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
   int* gids0 = reinterpret_cast<int*>(sm + L.gid);
   double* uxy = sm + L.uxy;
   double* stg = sm + L.stg;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + L.mbar);
+  unsigned mbar_phase = 0;
+  constexpr int OSTR = E * NP + 2;  // own staging array stride (TMA head alignment pad)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t K = a.K;
 
@@ -245,6 +267,10 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     }
     const int slots = E + gm8;
     for (int i = tid; i < slots * SU; i += NTHR) us[i] = 0.0;
+    if (MODE == MODE_PCG_A && tid == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     const int b = blockIdx.x;
     if (b < a.nblocks) {
       const int e0 = a.boff[b], Eb = a.boff[b + 1] - e0, g0 = a.goff[b], Gb = a.goff[b + 1] - g0;
@@ -278,6 +304,8 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     const int Gb = cur_Gb;
     short4* nbs = nbs0 + par * E;
     int* gids = gids0 + par * gm8;
+    int own_shift = 0;
+    bool use_tma = false;
     cp_async_wait_all();
     __syncthreads();  // previous block done with the buffers; this block's gids / nbr landed
     PHASE_MARK(0);  // wait for the previous block's stragglers + this block's metadata
@@ -297,17 +325,36 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
         cp_async8(us + (E + g) * SU + i, srcp + i);
       });
     } else {
-      double* sz = stg;                  // own: z | p_{k-1} | x, then ghosts: z | p_{k-1}
-      double* sp = stg + E * NP;
-      double* sx = stg + 2 * E * NP;
-      double* gz = stg + 3 * E * NP;
+      // own rows: one contiguous range per vector -> TMA bulk copies (16-byte aligned: the copy
+      // starts one double early when the range starts on an odd double; the tail block of the
+      // arrays falls back to cp.async)
+      double* sz = stg;                  // own: z | p_{k-1} | x (stride OSTR), then ghosts: z | p_{k-1}
+      double* sp = stg + OSTR;
+      double* sx = stg + 2 * OSTR;
+      double* gz = stg + 3 * OSTR;
       double* gp = gz + gm8 * NP;
-      for_rows<N>(Eb, warp, lane, [&](int e, int i) {
-        const int64_t g = (e0 + e) * NP + i;
-        cp_async8(sz + e * NP + i, a.z + g);
-        if (!first) cp_async8(sp + e * NP + i, pold + g);
-        if (do_xupd) cp_async8(sx + e * NP + i, a.x + g);
-      });
+      const int64_t g0 = e0 * NP;
+      own_shift = (int)(g0 & 1);
+      const int64_t gb = g0 - own_shift;
+      const unsigned nbytes = (unsigned)(((Eb * NP + own_shift) * 8 + 15) & ~15);
+      use_tma = (gb + nbytes / 8 <= K * NP);
+      if (use_tma) {
+        if (tid == 0) {
+          const unsigned tot = nbytes * (1u + (first ? 0u : 1u) + (do_xupd ? 1u : 0u));
+          mbar_expect_tx(mbar, tot);
+          tma_load_1d(sz, a.z + gb, nbytes, mbar);
+          if (!first) tma_load_1d(sp, pold + gb, nbytes, mbar);
+          if (do_xupd) tma_load_1d(sx, a.x + gb, nbytes, mbar);
+        }
+      } else {
+        own_shift = 0;
+        for_rows<N>(Eb, warp, lane, [&](int e, int i) {
+          const int64_t g = (e0 + e) * NP + i;
+          cp_async8(sz + e * NP + i, a.z + g);
+          if (!first) cp_async8(sp + e * NP + i, pold + g);
+          if (do_xupd) cp_async8(sx + e * NP + i, a.x + g);
+        });
+      }
       for_rows<N>(Gb, warp, lane, [&](int q, int i) {
         const int ge = gids[q];
         if (ge >= K) {
@@ -336,12 +383,16 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
       cp_async_commit();
     }
     cp_async_wait_group1();  // this block's data complete; the prefetch may still fly
+    if (MODE == MODE_PCG_A && use_tma) {
+      mbar_wait(mbar, mbar_phase);
+      mbar_phase ^= 1u;
+    }
     __syncthreads();
     if (MODE == MODE_PCG_A) {  // p_k = z + beta p_{k-1} (own + ghosts); x += alpha_{k-1} p_{k-1}
-      const double* sz = stg;
-      const double* sp = stg + E * NP;
-      const double* sx = stg + 2 * E * NP;
-      const double* gz = stg + 3 * E * NP;
+      const double* sz = stg + own_shift;
+      const double* sp = stg + OSTR + own_shift;
+      const double* sx = stg + 2 * OSTR + own_shift;
+      const double* gz = stg + 3 * OSTR;
       const double* gp = gz + gm8 * NP;
       for_rows<N>(Eb, warp, lane, [&](int e, int i) {
         const int o = e * NP + i;
