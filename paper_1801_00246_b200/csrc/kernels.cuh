@@ -43,7 +43,7 @@ struct Tr {
   static constexpr int pad416(int s) { return (s % 16 == 4 || s % 16 == 12) ? s : pad416(s + 1); }
   static constexpr int SU = pad416(NPK);         // smem row stride of u (conflict-free A loads)
   static constexpr int SF = pad416(KF);          // smem row stride of the face block
-  static constexpr int SXY = 2 * NPN + 2;        // smem row stride of (u_x | u_y) per slot (= 2 mod 16: gathers spread over banks)
+  static constexpr int SXY = 2 * NPN + 2;        // smem row stride of (w_r | w_s) per slot (= 2 mod 16: gathers spread over banks)
   static constexpr int SG = 8;                   // per-slot geometry: rx sx ry sy J det - -
   static constexpr int RPW = NP >= 32 ? 1 : 32 / NP;  // element rows copied per warp pass
   static constexpr int NPASS = (NP + 31) / 32;        // lane passes per row (NP > 32)

@@ -8,7 +8,8 @@
 //       formed from batched loads, p_k and the deferred x update written back);
 //       per-slot face geometry (J, det G, unit normals, sJ) computed once per slot
 //   P1  per 8-element tile: [u_r | u_s] = u [Dr^T | Ds^T] on DMMA      (Alg. AxG);
-//       u_x, u_y -> smem; own tiles keep w_r, w_s = J G (u_r, u_s) in registers (C layout)
+//       w_r, w_s = J G (u_r, u_s) -> smem (they also give the face normal derivatives) and, for
+//       own tiles, stay in registers (C layout) as the A operand of P3
 //   P2  per own face node: delta = u+ - u- (mirrored on boundary faces), flux
 //       g = 1/2 n-.(grad u- + grad u+) + tau delta                     (Alg. AxKernel)
 //       -> face block [1/2 sJ (n.grad r) delta | 1/2 sJ (n.grad s) delta | -sJ g]
@@ -77,7 +78,7 @@ __device__ unsigned long long ipdg_phase_cycles[8];
 
 // shared-memory layout (in doubles) shared by host and device
 struct SmemLayout {
-  int tabG, tabM, tabL, iaux, us, geo, fg, nb, gid, uxy, fa, stg, mbar, total;  // offsets in doubles
+  int tabG, tabM, tabL, iaux, us, geo, fg, nb, gid, wsm, stg, mbar, total;  // offsets in doubles
   template <int N>
   __host__ __device__ static SmemLayout make(int gmax, bool lam, bool pcg) {
     using T = Tr<N>;
@@ -97,11 +98,10 @@ struct SmemLayout {
     L.nb = o; o += 2 * T::E;            // short4 per element, double-buffered
     L.gid = o; o += gm8;                // 2 x gm8 ints, double-buffered
     o = (o + 1) & ~1;
-    L.uxy = o; o += slots * T::SXY;
-    L.fa = o;  // (face block lives in registers)
-    // PCG staging of r, D^-1, p_{k-1}, x (own) and r, D^-1, p_{k-1} (ghosts) aliases uxy / fa,
-    // which are produced only after the staging has been consumed
-    L.stg = L.uxy;
+    L.wsm = o; o += slots * T::SXY;     // w_r | w_s per slot (the face block lives in registers)
+    // PCG staging of z, p_{k-1}, x (own) and z, p_{k-1} (ghosts) aliases wsm, which is produced
+    // only after the staging has been consumed
+    L.stg = L.wsm;
     const int need = pcg ? 3 * (T::E * T::NP + 2) + 2 * gm8 * T::NP : 0;  // own arrays padded for TMA alignment
     if (L.stg + need > o) o = L.stg + need;
     L.mbar = o; o += 1;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
   double* fgs = sm + L.fg;
   short4* nbs0 = reinterpret_cast<short4*>(sm + L.nb);
   int* gids0 = reinterpret_cast<int*>(sm + L.gid);
-  double* uxy = sm + L.uxy;
+  double* wsm = sm + L.wsm;
   double* stg = sm + L.stg;
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + L.mbar);
   unsigned mbar_phase = 0;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
     }
 
     PHASE_MARK(1);  // P0: loads (and PCG prep)
-    // ---- P1: reference gradient on DMMA; u_x, u_y to smem; w_r / w_s kept for own tiles
+    // ---- P1: reference gradient on DMMA; w_r / w_s to smem, and kept in registers for own tiles
     const int ntiles = W + (Gb + 7) / 8;
     for (int t = warp; t < ntiles; t += W) {
       const bool own = t < W;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
       // normal derivatives at the face nodes: J g_f . grad u with g_f = -grad s, grad r + grad s,
       // -grad r gives sJ (n . grad u) = -w_s, w_r + w_s, -w_r on faces 0, 1, 2.
       const double Grr = J * (rx * rx + ry * ry), Grs = J * (rx * sx + ry * sy), Gss = J * (sx * sx + sy * sy);
-      double* wrow = uxy + srow * SXY + 2 * (lane & 3);
+      double* wrow = wsm + srow * SXY + 2 * (lane & 3);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const double ur0 = acc[nt][0], ur1 = acc[nt][1], us0 = acc[NT + nt][0], us1 = acc[NT + nt][1];
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
         const int ec = e < Eb ? e : 8 * warp;  // rows past the block end compute on a valid slot, never stored
         const short4 nb = nbs[ec];
         const double* uo = us + ec * SU;
-        const double* wo = uxy + ec * SXY;
+        const double* wo = wsm + ec * SXY;
         const double* fq0 = fgs + ec;
 #pragma unroll
         for (int q = 0; q < T::NQ; ++q) {
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
             const int ps = inner ? slot : ec;
             const int pf = inner ? fp : f;
             const int ip = inner ? nidx[(2 * fp + ((f == 2) == (fp == 2))) * NFP + kk] : i;
-            const double* wn = uxy + ps * SXY;
+            const double* wn = wsm + ps * SXY;
             const double um = uo[i], upr = us[ps * SU + ip];
             // sJ n.grad u at the node: -w_s, w_r + w_s, -w_r on faces 0, 1, 2 (own normal for u-,
             // the neighbour's own normal for u+, hence the sign flip below)
