@@ -247,6 +247,8 @@ def run_ours(args):
         op = Ipdg.distributed(N, mesh, part, rank, world, device=local)
     else:
         op = Ipdg(N, mesh, device=local)
+    if args.variant:
+        op.set_variant(args.variant)
     K, Np = op.K, op.Np
     # right-hand side b = J M f_I of the manufactured problem (setup, not timed)
     x_nodes, y_nodes = op.nodes()
@@ -420,7 +422,7 @@ def run_sweep(args):
     nx = args.sweep_nx
     mesh = meshgen.square(nx, jitter=0.2, diag="random", order="morton", seed=3)
     stream = torch.cuda.current_stream()
-    for N, variant in [(N, v) for N in range(1, 9) for v in args.sweep_variants]:
+    for N, variant in [(N, v) for N in range(1, 9) for v in args.sweep_variants if v != 3 or N <= 4]:
         op = Ipdg(N, mesh)
         op.set_variant(variant)
         K, Np = op.K, op.Np
@@ -467,9 +469,10 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=600)
     ap.add_argument("--cpu-nx", type=int, default=100)
     ap.add_argument("--ref-nx", type=int, default=50)
+    ap.add_argument("--variant", type=int, default=0, help="operator kernel variant (0 auto)")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-nx", type=int, default=707)
-    ap.add_argument("--sweep-variants", type=int, nargs="+", default=[0], help="0 auto, 1 fused, 2 split")
+    ap.add_argument("--sweep-variants", type=int, nargs="+", default=[0], help="0 auto, 1 fused, 2 split, 3 thread-per-element (N<=4)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

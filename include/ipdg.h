@@ -170,8 +170,10 @@ int ipdg_get_geofacs(ipdg_ctx ctx, double* host, int64_t cap);
 int ipdg_get_connectivity(ipdg_ctx ctx, int32_t* etoe, int32_t* etof, int64_t cap);
 /* out[0..n): N, Np, K, nblocks, E (own elements per block), Gmax, smem bytes/CTA, grid */
 int ipdg_info(ipdg_ctx ctx, int64_t* out, int n);
-/* Operator kernel variant: 0 auto (fused for N <= 5, split for N >= 6), 1 fused single-kernel
- * (k_sipdg), 2 split gradient + flux kernels (k_grad, k_flux).  Results agree to rounding. */
+/* Operator kernel variant: 0 auto (the variant measured fastest for the degree), 1 fused
+ * single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels (k_grad, k_flux, DMMA),
+ * 3 thread-per-element (k_tpe, DFMA with operators in constant memory; N <= 4 only, else
+ * IPDG_EINVAL).  Results agree to rounding.  Switching drops captured CG graphs. */
 int ipdg_set_variant(ipdg_ctx ctx, int variant);
 /* number of kernel launches this context has issued (evidence counter) */
 int64_t ipdg_launch_count(ipdg_ctx ctx);

@@ -11,7 +11,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["ipdg.cu", "refops.cpp"]
-DEPS = SOURCES + ["kernels.cuh", "sipdg_kernels.cuh", "refops.h"]
+DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _stale():

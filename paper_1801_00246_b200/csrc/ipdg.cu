@@ -32,6 +32,7 @@
 #include "refops.h"
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
+#include "sipdg_tpe.cuh"
 
 using namespace ipdg;
 
@@ -59,7 +60,13 @@ struct ipdg_ctx_s {
   // split variant (k_grad + k_flux): neighbour ids per element, W = [w_r | w_s] scratch
   int4* nbg = nullptr;
   double* W2 = nullptr;
-  int variant = 0;  // 0 auto (split for N >= 6), 1 fused, 2 split
+  int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4)
+  // thread-per-element variant (k_tpe): its own block schedule
+  int t_nblocks = 0;
+  int *t_boff = nullptr, *t_goff = nullptr, *t_gid = nullptr;
+  short4* t_nbr = nullptr;
+  size_t smem_tpe[2] = {0, 0};
+  int grid_tpe[2][2] = {{0, 0}, {0, 0}};
   size_t smem_grad = 0, smem_flux[2] = {0, 0};
   int grid_grad = 0, grid_flux[2][2] = {{0, 0}, {0, 0}};
   size_t smem[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
@@ -318,11 +325,115 @@ struct Impl {
         c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
       }
     }
+    return configure_tpe(c, optin);
+  }
+
+  // ---- thread-per-element variant (N <= 4)
+  static int configure_tpe(ipdg_ctx c, int optin) {
+    if constexpr (N <= 4) {
+      using TT = TrT<N>;
+      for (int mode = 0; mode < 2; ++mode) {
+        const size_t bytes = (size_t)(mode == 1 ? TpeSmem<N, true>::total() : TpeSmem<N, false>::total()) * sizeof(double);
+        c->smem_tpe[mode] = bytes;
+        for (int lam = 0; lam < 2; ++lam) {
+          const void* fn = (mode == 0) ? (lam ? (const void*)k_tpe<N, MODE_AX, true> : (const void*)k_tpe<N, MODE_AX, false>)
+                                       : (lam ? (const void*)k_tpe<N, MODE_PCG_A, true> : (const void*)k_tpe<N, MODE_PCG_A, false>);
+          CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+          int o = 0;
+          CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, TT::NTHR, bytes));
+          c->grid_tpe[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>(c->t_nblocks, (int64_t)std::max(1, o) * c->sms));
+        }
+      }
+    }
     return IPDG_OK;
   }
 
-  // auto: the faster variant measured per degree on C3 (profiles/r01_sweep_variants.jsonl)
-  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && !(N == 2 || N == 4 || N == 5)); }
+  static int upload_tpe_constants(ipdg_ctx c) {
+    if constexpr (N <= 4) {
+      using TT = TrT<N>;
+      const RefOps& R = c->ref;
+      const int NP = TT::NP, NFP = TT::NFP, NF3 = TT::NF3;
+      std::vector<double> h(TT::TOTAL, 0.0);
+      for (int i = 0; i < NP * NP; ++i) {
+        h[TT::O_DR + i] = R.Dr[i];
+        h[TT::O_DS + i] = R.Ds[i];
+        h[TT::O_SR + i] = R.Sr[i];
+        h[TT::O_SS + i] = R.Ss[i];
+        h[TT::O_M + i] = R.M[i];
+      }
+      for (int m = 0; m < NF3; ++m)
+        for (int n = 0; n < NP; ++n) {
+          double a = 0, b = 0;
+          for (int i = 0; i < NP; ++i) {
+            a += R.LIFT[i * NF3 + m] * R.Sr[i * NP + n];
+            b += R.LIFT[i * NF3 + m] * R.Ss[i * NP + n];
+          }
+          h[TT::O_LSR + m * NP + n] = a;
+          h[TT::O_LSS + m * NP + n] = b;
+        }
+      for (int i = 0; i < NFP * NFP; ++i) h[TT::O_M1D + i] = R.M1D[i];
+      CUDA_TRY(c, cudaMemcpyToSymbol(c_tpe<N>, h.data(), h.size() * sizeof(double)));
+    }
+    return IPDG_OK;
+  }
+
+  static TpeArgs targs(ipdg_ctx c) {
+    TpeArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.K = c->K;
+    a.nblocks = c->t_nblocks;
+    a.boff = c->t_boff;
+    a.goff = c->t_goff;
+    a.gid = c->t_gid;
+    a.nbr = c->t_nbr;
+    a.geo = c->geo;
+    a.tau_c = c->tau_c;
+    a.halo = c->halobuf;
+    return a;
+  }
+
+  static int ax_tpe(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
+    if constexpr (N <= 4) {
+      TpeArgs a = targs(c);
+      a.u = u;
+      a.Au = Au;
+      a.lambda = lambda;
+      if (lambda != 0.0) k_tpe<N, MODE_AX, true><<<c->grid_tpe[0][1], TrT<N>::NTHR, c->smem_tpe[0], s>>>(a);
+      else k_tpe<N, MODE_AX, false><<<c->grid_tpe[0][0], TrT<N>::NTHR, c->smem_tpe[0], s>>>(a);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    } else {
+      FAIL(c, IPDG_EINVAL, "thread-per-element variant needs N <= 4");
+    }
+  }
+
+  static int pass_a_tpe(ipdg_ctx c, cudaStream_t s) {
+    if constexpr (N <= 4) {
+      TpeArgs a = targs(c);
+      a.lambda = c->lambda;
+      a.z = c->precond ? c->zb : c->r;
+      a.p_even = c->pe;
+      a.p_odd = c->po;
+      a.x = c->x;
+      a.Au = c->Ap;
+      a.st = c->st;
+      a.partials = c->partials;
+      a.counter = c->counter;
+      if (c->lambda != 0.0) k_tpe<N, MODE_PCG_A, true><<<c->grid_tpe[1][1], TrT<N>::NTHR, c->smem_tpe[1], s>>>(a);
+      else k_tpe<N, MODE_PCG_A, false><<<c->grid_tpe[1][0], TrT<N>::NTHR, c->smem_tpe[1], s>>>(a);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    } else {
+      FAIL(c, IPDG_EINVAL, "thread-per-element variant needs N <= 4");
+    }
+  }
+
+  // auto (variant 0): thread-per-element for N <= 3, fused for N = 4, 5, split for N >= 6 -- the
+  // fastest per degree on C3 (profiles/r01_sweep_variants_tpe.jsonl)
+  static bool use_tpe(ipdg_ctx c) { return c->variant == 3 || (c->variant == 0 && N <= 3); }
+  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
 
   static SplitArgs sargs(ipdg_ctx c) {
     SplitArgs a;
@@ -399,6 +510,7 @@ struct Impl {
   }
 
   static int ax(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
+    if (use_tpe(c)) return ax_tpe(c, u, Au, lambda, s);
     if (use_split(c)) return ax_split(c, u, Au, lambda, s);
     AxArgs a = args(c);
     a.u = u;
@@ -414,6 +526,7 @@ struct Impl {
   }
 
   static int pass_a(ipdg_ctx c, cudaStream_t s) {
+    if (use_tpe(c)) return pass_a_tpe(c, s);
     if (use_split(c)) return pass_a_split(c, s);
     AxArgs a = args(c);
     a.lambda = c->lambda;
@@ -522,11 +635,13 @@ static int upload(ipdg_ctx c, Tp** dst, const Tp* src, size_t n) {
 }
 
 static void free_mesh(ipdg_ctx c) {
-  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2};
+  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
+                  c->t_boff, c->t_goff, c->t_gid, c->t_nbr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->geo = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
   c->nbg = nullptr; c->W2 = nullptr;
+  c->t_boff = nullptr; c->t_goff = nullptr; c->t_gid = nullptr; c->t_nbr = nullptr; c->t_nblocks = 0;
   c->bcode = nullptr;
   c->vxy = nullptr;
   for (auto& g : c->gexec)
@@ -611,6 +726,10 @@ int ipdg_create(ipdg_ctx* out, int N, int device) {
   for (int i = 0; i < R.Np; ++i) { rs[i] = R.r[i]; rs[R.Np + i] = R.s[i]; }
   if ((rc = upload(c, &c->tables, tab.data(), tab.size())) || (rc = upload(c, &c->diagtab, dtab.data(), dtab.size())) ||
       (rc = upload(c, &c->rs, rs.data(), rs.size())) || (rc = upload(c, &c->Mref, R.M.data(), R.M.size()))) {
+    delete c;
+    return rc;
+  }
+  if ((rc = [&]() -> int { DISPATCH(N, upload_tpe_constants(c)); }())) {
     delete c;
     return rc;
   }
@@ -701,21 +820,21 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
 
 // Block schedule, device arrays, geometric factors and launch configuration for the mesh
 // stored by ipdg_upload_mesh plus H halo ghosts (ghost element g has local id K + g).
-static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
-  const int64_t K = c->pend_K;
-  const int E = c->E;
-  std::vector<int>& etoe = c->pend_etoe;
-  std::vector<int>& etof = c->pend_etof;
-  const int8_t* bc = c->pend_bc.data();
-  // ---- element blocks and ghost lists.  A block is a contiguous range of at most E own
-  // elements whose distinct outside face neighbours (ghosts) fit the shared-memory budget
-  // gcap; well-ordered meshes (Morton, RCB) never hit the cap, scattered orderings get
-  // shorter blocks instead of failing.  Halo ghosts (id >= K) are ordinary ghosts whose
-  // values come from the received halo buffer.
-  const int gcap = ghost_cap(c->N, c->device);
-  std::vector<int> goff(1, 0), gid, boff(1, 0);
-  std::vector<short4> nbr(K);
+// Element-block schedule: contiguous ranges of at most E own elements whose distinct outside face
+// neighbours (ghosts) fit the budget gcap.  Well-ordered meshes (Morton, RCB) never hit the cap,
+// scattered orderings get shorter blocks instead of failing.  Halo ghosts (id >= K) are ordinary
+// ghosts whose values come from the received halo buffer.  Slots: own e - e0, ghosts E + index.
+struct Schedule {
+  std::vector<int> boff, goff, gid;
+  std::vector<short4> nbr;
   int gmax = 0;
+};
+static Schedule build_schedule(int64_t K, int E, int gcap, const std::vector<int>& etoe, const std::vector<int>& etof,
+                               const int8_t* bc) {
+  Schedule S;
+  S.boff.assign(1, 0);
+  S.goff.assign(1, 0);
+  S.nbr.resize(K);
   std::vector<int> gl;
   int64_t e0 = 0;
   while (e0 < K) {
@@ -743,7 +862,7 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
       }
       ++e1;
     }
-    gmax = std::max<int>(gmax, (int)gl.size());
+    S.gmax = std::max<int>(S.gmax, (int)gl.size());
     for (int64_t e = e0; e < e1; ++e) {
       short sl[3] = {0, 0, 0};
       int flags = 0;
@@ -759,12 +878,35 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
         const int code = (bc[e * 3 + f] == IPDG_BC_REMOTE) ? IPDG_BC_INTERIOR : bc[e * 3 + f];
         flags |= ((fp & 3) | ((code & 3) << 2)) << (4 * f);
       }
-      nbr[e] = make_short4(sl[0], sl[1], sl[2], (short)flags);
+      S.nbr[e] = make_short4(sl[0], sl[1], sl[2], (short)flags);
     }
-    gid.insert(gid.end(), gl.begin(), gl.end());
-    goff.push_back((int)gid.size());
-    boff.push_back((int)e1);
+    S.gid.insert(S.gid.end(), gl.begin(), gl.end());
+    S.goff.push_back((int)S.gid.size());
+    S.boff.push_back((int)e1);
     e0 = e1;
+  }
+  return S;
+}
+
+static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
+  const int64_t K = c->pend_K;
+  const int E = c->E;
+  std::vector<int>& etoe = c->pend_etoe;
+  std::vector<int>& etof = c->pend_etof;
+  const int8_t* bc = c->pend_bc.data();
+  Schedule S = build_schedule(K, E, ghost_cap(c->N, c->device), etoe, etof, bc);
+  std::vector<int>& boff = S.boff;
+  std::vector<int>& goff = S.goff;
+  std::vector<int>& gid = S.gid;
+  std::vector<short4>& nbr = S.nbr;
+  const int gmax = S.gmax;
+  if (c->N <= 4) {  // thread-per-element variant: its own blocks (E = 128, <= 64 ghosts)
+    Schedule T = build_schedule(K, 128, 64, etoe, etof, bc);
+    c->t_nblocks = (int)T.boff.size() - 1;
+    TRY(upload(c, &c->t_boff, T.boff.data(), T.boff.size()));
+    TRY(upload(c, &c->t_goff, T.goff.data(), T.goff.size()));
+    TRY(upload(c, &c->t_gid, T.gid.data(), T.gid.size()));
+    TRY(upload(c, &c->t_nbr, T.nbr.data(), T.nbr.size()));
   }
   const int nb = (int)boff.size() - 1;
   if (E + gmax > 32000) FAIL(c, IPDG_EMESH, "element ordering too scattered (a block has %d ghosts)", gmax);
@@ -1354,7 +1496,7 @@ int ipdg_debug_phase_cycles(unsigned long long* out8, int reset) {
 }
 
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 2) return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 3 || (variant == 3 && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

@@ -18,9 +18,8 @@ def _mesh():
                           tag=lambda x, y: np.where(y > 0.4, 1, 2).astype(np.int8))
 
 
-@pytest.mark.parametrize("N", [1, 4, 6, 8])
+@pytest.mark.parametrize("N,variant", [(1, 1), (4, 1), (6, 1), (8, 1), (1, 2), (4, 2), (6, 2), (8, 2), (2, 3), (4, 3)])
 @pytest.mark.parametrize("P", [2, 3])
-@pytest.mark.parametrize("variant", [1, 2])
 def test_partitioned_ax_loopback(N, P, variant):
     m = _mesh()
     part = meshgen.rcb_partition(m["VX"], m["VY"], m["EToV"], P)

@@ -153,10 +153,10 @@ def test_full_size_c2_parity(N):
     assert err.max() <= 1e-11
 
 
-@pytest.mark.parametrize("N", range(1, 9))
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("N,variant", [(N, v) for N in range(1, 9) for v in (1, 2, 3) if v < 3 or N <= 4])
 def test_ax_kernel_variants(N, variant):
-    """Fused k_sipdg (variant 1) and split k_grad + k_flux (variant 2) both match the oracle."""
+    """Fused k_sipdg (variant 1), split k_grad + k_flux (variant 2) and thread-per-element k_tpe
+    (variant 3, N <= 4) all match the oracle."""
     m = MESHES["mixed_bc"]()
     ref = RefElem(N)
     op = Ipdg(N, m)
@@ -166,6 +166,26 @@ def test_ax_kernel_variants(N, variant):
         u = meshgen.uniform_field(op.K, op.Np, seed=200 + N)
         Au = op.ax(gpu(u), lam=lam).cpu().numpy()
         assert rel(Au.ravel(), A @ u.ravel()) <= TOL, (N, variant, lam)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4])
+@pytest.mark.parametrize("mesh", ["random_order", "ragged", "tiny"])
+def test_ax_tpe_meshes(N, mesh):
+    """k_tpe on scattered orderings (short blocks at the 64-ghost cap), ragged and tiny meshes."""
+    m = MESHES[mesh]()
+    op = Ipdg(N, m)
+    op.set_variant(3)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], RefElem(N))
+    u = meshgen.uniform_field(op.K, op.Np, seed=300 + N)
+    Au = op.ax(gpu(u)).cpu().numpy()
+    assert rel(Au.ravel(), A @ u.ravel()) <= TOL
+
+
+def test_tpe_variant_rejected_for_high_degree():
+    m = MESHES["tiny"]()
+    op = Ipdg(5, m)
+    with pytest.raises(IpdgError):
+        op.set_variant(3)
 
 
 def _extended_oracle(m, elems, N):
