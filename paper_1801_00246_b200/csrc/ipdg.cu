@@ -33,6 +33,7 @@
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
 #include "sipdg_tpe.cuh"
+#include "sipdg_pipe.cuh"
 
 using namespace ipdg;
 
@@ -60,7 +61,10 @@ struct ipdg_ctx_s {
   // split variant (k_grad + k_flux): neighbour ids per element, W = [w_r | w_s] scratch
   int4* nbg = nullptr;
   double* W2 = nullptr;
-  int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4)
+  int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4), 4 pipelined fused
+  // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit
+  size_t smem_pipe[2][2] = {{0, 0}, {0, 0}};
+  int grid_pipe[2][2] = {{0, 0}, {0, 0}};
   // thread-per-element variant (k_tpe): its own block schedule
   int t_nblocks = 0;
   int *t_boff = nullptr, *t_goff = nullptr, *t_gid = nullptr;
@@ -325,7 +329,27 @@ struct Impl {
         c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
       }
     }
+    TRY(configure_pipe(c, optin));
     return configure_tpe(c, optin);
+  }
+
+  // ---- pipelined fused variant: needs room for the staging area next to the working rows
+  static int configure_pipe(ipdg_ctx c, int optin) {
+    for (int lam = 0; lam < 2; ++lam)
+      for (int mode = 0; mode < 2; ++mode) {
+        const PipeLayout L = PipeLayout::make<N>(c->gmax, lam != 0, mode == 1);
+        const size_t bytes = (size_t)L.total * sizeof(double);
+        c->smem_pipe[mode][lam] = bytes;
+        c->grid_pipe[mode][lam] = 0;
+        if ((int)bytes > optin - 1024) continue;
+        const void* fn = (mode == 0) ? (lam ? (const void*)k_pipe<N, MODE_AX, true> : (const void*)k_pipe<N, MODE_AX, false>)
+                                     : (lam ? (const void*)k_pipe<N, MODE_PCG_A, true> : (const void*)k_pipe<N, MODE_PCG_A, false>);
+        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        int occ = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
+        if (occ >= 1) c->grid_pipe[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
+      }
+    return IPDG_OK;
   }
 
   // ---- thread-per-element variant (N <= 4)
@@ -434,6 +458,7 @@ struct Impl {
   // fastest per degree on C3 (profiles/r01_sweep_variants_tpe.jsonl)
   static bool use_tpe(ipdg_ctx c) { return c->variant == 3 || (c->variant == 0 && N <= 3); }
   static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
+  static bool use_pipe(ipdg_ctx c, int mode, bool lam) { return c->variant == 4 && c->grid_pipe[mode][lam] > 0; }
 
   static SplitArgs sargs(ipdg_ctx c) {
     SplitArgs a;
@@ -517,6 +542,14 @@ struct Impl {
     a.Au = Au;
     a.lambda = lambda;
     const bool lam = lambda != 0.0;
+    if (use_pipe(c, 0, lam)) {
+      const int gp = c->grid_pipe[0][lam];
+      if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
+      else k_pipe<N, MODE_AX, false><<<gp, T::W * 32, c->smem_pipe[0][0], s>>>(a, c->gmax);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    }
     const int g = c->grid[0][lam];
     if (lam) k_sipdg<N, MODE_AX, true><<<g, T::W * 32, c->smem[0][1], s>>>(a, c->gmax);
     else k_sipdg<N, MODE_AX, false><<<g, T::W * 32, c->smem[0][0], s>>>(a, c->gmax);
@@ -541,6 +574,14 @@ struct Impl {
     a.partials = c->partials;
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
+    if (use_pipe(c, 1, lam)) {
+      const int gp = c->grid_pipe[1][lam];
+      if (lam) k_pipe<N, MODE_PCG_A, true><<<gp, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
+      else k_pipe<N, MODE_PCG_A, false><<<gp, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    }
     const int g = c->grid[1][lam];
     if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1][1], s>>>(a, c->gmax);
     else k_sipdg<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem[1][0], s>>>(a, c->gmax);
@@ -1496,7 +1537,7 @@ int ipdg_debug_phase_cycles(unsigned long long* out8, int reset) {
 }
 
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 3 || (variant == 3 && c->N > 4)) return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 4 || (variant == 3 && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

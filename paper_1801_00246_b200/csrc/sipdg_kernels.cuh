@@ -15,6 +15,7 @@
 //       -> face block [1/2 sJ (n.grad r) delta | 1/2 sJ (n.grad s) delta | -sJ g]
 //   P3  per own tile: Au = [w_r | w_s | face block] x [Sr; Ss; LIFT^T Sr; LIFT^T Ss; E^T] on DMMA
 //       (+ lambda J u M), stored element-major; PCG pass A also accumulates p . Ap.
+#pragma once
 #include "kernels.cuh"
 
 namespace ipdg {
