@@ -45,6 +45,8 @@ struct ipdg_ctx_s {
   bool has_dirichlet = false;
   // device mesh data
   double4* geo = nullptr;
+  double4* gG = nullptr;  // per-element J G^T G records (k_pipe)
+  double* gF = nullptr;   // per-face lift coefficients and sJ tau (k_pipe)
   short4* nbr = nullptr;
   int* goff = nullptr;
   int* gid = nullptr;
@@ -92,6 +94,7 @@ struct ipdg_ctx_s {
   double* x = nullptr;
   double lambda = 0.0;
   int precond = 0;
+  bool xb = false;  // pass B updates x (k_pipe pass A); else pass A applies the deferred update
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0]: 1 iteration, [1]: kChunk iterations
   const void* gkey_x = nullptr;
   double gkey_lambda = -1.0;
@@ -338,7 +341,7 @@ struct Impl {
     for (int lam = 0; lam < 2; ++lam)
       for (int mode = 0; mode < 2; ++mode) {
         const PipeLayout L = PipeLayout::make<N>(c->gmax, lam != 0, mode == 1);
-        const size_t bytes = (size_t)L.total * sizeof(double);
+        const size_t bytes = (size_t)L.total() * sizeof(double);
         c->smem_pipe[mode][lam] = bytes;
         c->grid_pipe[mode][lam] = 0;
         if ((int)bytes > optin - 1024) continue;
@@ -458,7 +461,11 @@ struct Impl {
   // fastest per degree on C3 (profiles/r01_sweep_variants_tpe.jsonl)
   static bool use_tpe(ipdg_ctx c) { return c->variant == 3 || (c->variant == 0 && N <= 3); }
   static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
-  static bool use_pipe(ipdg_ctx c, int mode, bool lam) { return c->variant == 4 && c->grid_pipe[mode][lam] > 0; }
+  // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
+  static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+  static bool use_pipe(ipdg_ctx c, int mode, bool lam, const void* v) {
+    return c->variant == 4 && c->grid_pipe[mode][lam] > 0 && aligned16(v);
+  }
 
   static SplitArgs sargs(ipdg_ctx c) {
     SplitArgs a;
@@ -522,6 +529,7 @@ struct Impl {
     AxArgs a;
     std::memset(&a, 0, sizeof(a));
     a.K = c->K;
+    a.H = c->H;
     a.nblocks = c->nblocks;
     a.geo = c->geo;
     a.nbr = c->nbr;
@@ -529,6 +537,8 @@ struct Impl {
     a.gid = c->gid;
     a.boff = c->boff;
     a.tables = c->tables;
+    a.gG = c->gG;
+    a.gF = c->gF;
     a.tau_c = c->tau_c;
     a.halo_p = c->halobuf;
     return a;
@@ -542,7 +552,7 @@ struct Impl {
     a.Au = Au;
     a.lambda = lambda;
     const bool lam = lambda != 0.0;
-    if (use_pipe(c, 0, lam)) {
+    if (use_pipe(c, 0, lam, u)) {
       const int gp = c->grid_pipe[0][lam];
       if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
       else k_pipe<N, MODE_AX, false><<<gp, T::W * 32, c->smem_pipe[0][0], s>>>(a, c->gmax);
@@ -569,12 +579,13 @@ struct Impl {
     a.p_even = c->pe;
     a.p_odd = c->po;
     a.x = c->x;
+    a.defer_x = c->xb ? 0 : 1;
     a.Au = c->Ap;
     a.st = c->st;
     a.partials = c->partials;
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
-    if (use_pipe(c, 1, lam)) {
+    if (use_pipe(c, 1, lam, c->x)) {
       const int gp = c->grid_pipe[1][lam];
       if (lam) k_pipe<N, MODE_PCG_A, true><<<gp, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
       else k_pipe<N, MODE_PCG_A, false><<<gp, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
@@ -676,11 +687,11 @@ static int upload(ipdg_ctx c, Tp** dst, const Tp* src, size_t n) {
 }
 
 static void free_mesh(ipdg_ctx c) {
-  void* ptrs[] = {c->geo, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
+  void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
                   c->t_boff, c->t_goff, c->t_gid, c->t_nbr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  c->geo = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
+  c->geo = nullptr; c->gG = nullptr; c->gF = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
   c->nbg = nullptr; c->W2 = nullptr;
   c->t_boff = nullptr; c->t_goff = nullptr; c->t_gid = nullptr; c->t_nbr = nullptr; c->t_nblocks = 0;
   c->bcode = nullptr;
@@ -988,6 +999,11 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   CUDA_TRY(c, cudaMemcpy(&badh, bad, sizeof(badh), cudaMemcpyDeviceToHost));
   cudaFree(bad);
   if (badh != none) FAIL(c, IPDG_EMESH, "element %llu has J <= 0 (vertices must be counter-clockwise)", badh);
+  CUDA_TRY(c, cudaMalloc(&c->gG, KH * sizeof(double4)));
+  CUDA_TRY(c, cudaMalloc(&c->gF, std::max<int64_t>(1, K) * 12 * sizeof(double)));
+  k_geofacs<<<(unsigned)((KH + 255) / 256), 256>>>(K, KH, c->geo, c->etoe, c->bcode, c->tau_c, c->gG, c->gF);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
   DISPATCH(c->N, configure(c));
 }
 
@@ -1231,7 +1247,7 @@ static int one_iteration(ipdg_ctx c, cudaStream_t s) {
   TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
   TRY(allreduce(c, &c->st->red_A, 1, s));
   k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
-                                        c->st, c->partials, c->counter);
+                                        c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   TRY(allreduce(c, c->st->red_B, 2, s));
@@ -1274,6 +1290,9 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   c->x = x;
   c->lambda = lambda;
   c->precond = precond;
+  // x is updated by pass A (deferred x += alpha_{k-1} p_{k-1}).  The alternative protocol, x += alpha_k p_k
+  // in pass B (k_pcg_b with x), measured slower on C2 with k_pipe (pass B 18 -> 29 us, pass A -3 us).
+  c->xb = false;
   PcgState h;
   std::memset(&h, 0, sizeof(h));
   h.tol2 = tol * tol;
@@ -1342,7 +1361,8 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b,
       if ((rc = allreduce(c, &c->st->red_A, 1, s)) != IPDG_OK) break;
       cudaEventRecord(ev[3 * i + 1], s);
       k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
-                                            c->st, c->partials, c->counter);
+                                            c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe,
+                                            c->po);
       c->launches++;
       cudaEventRecord(ev[3 * i + 2], s);
       if ((rc = allreduce(c, c->st->red_B, 2, s)) != IPDG_OK) break;
@@ -1371,9 +1391,12 @@ int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
   if (!c->x) FAIL(c, IPDG_ESTATE, "ipdg_pcg_end before ipdg_pcg_begin");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = c->K * c->ref.Np;
-  k_pcg_final_x<<<vec_grid(c), 256, 0, s>>>(n, c->x, c->pe, c->po, c->st);
+  if (!c->xb) {
+    k_pcg_final_x<<<vec_grid(c), 256, 0, s>>>(n, c->x, c->pe, c->po, c->st);
+    c->launches++;
+  }
   k_pcg_final_state<<<1, 1, 0, s>>>(c->st);
-  c->launches += 2;
+  c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));

@@ -70,6 +70,7 @@ __host__ __device__ __forceinline__ constexpr int fmask_cf(int f, int k) {
 // Kernel parameters (plain pointers; all device memory).
 struct AxArgs {
   int64_t K;             // local elements
+  int64_t H;             // halo ghosts (rows of halo_p)
   int nblocks;           // element blocks (contiguous ranges of <= E own elements)
   const int* boff;       // [nblocks+1] first element of each block
   const double4* geo;    // [K + H] r_x, s_x, r_y, s_y  (H = halo ghosts, multi-GPU)
@@ -77,6 +78,8 @@ struct AxArgs {
   const int* goff;       // [nblocks+1] ghost list offsets
   const int* gid;        // ghost element ids (>= K: halo index K + h)
   const double* tables;  // fragment tables: G | M | L
+  const double4* gG;     // [K + H] (J G_rr, J G_rs, J G_ss, J) per element (k_pipe)
+  const double* gF;      // [K][12] per face (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau) (k_pipe)
   double tau_c;          // (N+1)(N+2)/2 * tau_scale
   double lambda;
   // MODE_AX
@@ -89,6 +92,7 @@ struct AxArgs {
   double* p_even;        // p_k lives in p_even when k is even, p_odd when k is odd
   double* p_odd;         //   (double buffer: ghosts read p_{k-1} while owners write p_k)
   double* x;             // deferred update x += alpha_{k-1} p_{k-1}
+  int defer_x;           // k_pipe: 1 = pass A applies the deferred x update, 0 = pass B updates x
   const double* halo_p;  // [H x NP] received ghost values of p_k (multi-GPU), else null
   struct PcgState* st;
   double* partials;      // [gridDim.x]

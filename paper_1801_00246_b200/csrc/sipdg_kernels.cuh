@@ -588,9 +588,11 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
 }
 
 // ---- PCG pass B: r -= alpha A p; z = D^{-1} r; partial (r.z, r.r)
+// With x != null (k_pipe protocol) it also applies x += alpha_k p_k (p_k from pass A of this iteration)
 __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r, const double* __restrict__ Ap,
                                                const double* __restrict__ dinv, double* __restrict__ z, PcgState* st,
-                                               double* partials, unsigned int* counter) {
+                                               double* partials, unsigned int* counter, double* __restrict__ x,
+                                               const double* p_even, const double* p_odd) {
   __shared__ double red[32 * 3];
   if (st->stop_iter >= 0) return;
   const long long k = st->it + 1;
@@ -607,8 +609,10 @@ __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r
     return;
   }
   const double alpha = rho / sigma;
+  const double* __restrict__ p = (k & 1) ? p_odd : p_even;
   double rz = 0.0, rr = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (x) x[i] = fma(alpha, p[i], x[i]);
     const double ri = r[i] - alpha * Ap[i];
     r[i] = ri;
     const double zi = dinv ? ri * dinv[i] : ri;

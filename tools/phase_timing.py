@@ -20,11 +20,13 @@ lib = L.lib()
 fn = lib.ipdg_debug_phase_cycles
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 8)()
-names = ["top-wait", "P0 loads", "P1 grad", "P2 faces", "P3 gemm", "P3 store"]
+variant = int(os.environ.get("VARIANT", "1"))
+names = (["top-wait", "P0 loads", "P1 grad", "P2 faces", "P3 gemm", "P3 store"] if variant == 1 else
+         ["top-wait", "issue", "p/x stores", "P1+vol", "barrier", "P2/P3+store"])
 for N in [int(a) for a in sys.argv[1:]] or [4]:
     mesh = meshgen.square(316, jitter=0.2, diag="random", order="morton", seed=2)
     op = Ipdg(N, mesh)
-    op.set_variant(1)
+    op.set_variant(variant)
     u = torch.rand(op.K, op.Np, dtype=torch.float64, device="cuda")
     op.ax(u)
     torch.cuda.synchronize()
