@@ -39,6 +39,7 @@ def peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
+KERNEL_NAMES = {1: "k_sipdg", 2: "k_grad+k_flux", 3: "k_tpe", 4: "k_pipe"}
 FP64_PEAK_TFLOPS = 36.8  # measured DFMA / DMMA peak on this pool's B200 (profiles/r01_micro_fp64.jsonl)
 
 
@@ -176,12 +177,12 @@ def ax_flops_per_elem(N):
     return 8 * Np * Np + 6 * Np * Nfp + 6 * Nfp * Nfp + 18 * Np + 36 * Nfp  # F_min
 
 
-def traffic_from_profile(N, K):
+def traffic_from_profile(N, K, kernel):
     """dram bytes per launch of pass A from the committed ncu capture (profiles/), or None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         e = d["pass_a"]
-        if e.get("N") == N and e.get("K") == K:
+        if e.get("N") == N and e.get("K") == K and e.get("kernel", "k_sipdg") == kernel:
             return e["dram_bytes_per_launch"]
     except Exception:
         pass
@@ -349,8 +350,9 @@ def run_ours(args):
                    "l2": "working set 6 x K x Np x 8 B = %.0f MB > 126 MB L2 (no flush needed)" % (6 * 8 * K * Np / 1e6),
                    "parallelism": "element partition, %d rank(s)" % world},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                     "frac": round(achieved / pk.get("hbm_gbs"), 4), "traffic": traffic_from_profile(N, K),
-                     "kernel": "k_sipdg<N=4, PCG pass A>", "avg_launch_ms": round(avg_a, 5),
+                     "frac": round(achieved / pk.get("hbm_gbs"), 4), "traffic": traffic_from_profile(N, K, KERNEL_NAMES.get(info.get("kernel"))),
+                     "kernel": "%s<N=%d, PCG pass A>" % (KERNEL_NAMES.get(info.get("kernel"), "?"), N),
+                     "avg_launch_ms": round(avg_a, 5),
                      "algorithmic_bytes_per_launch": bytes_a, "share_of_step": round(share_a, 3),
                      "fp64_tflops": round(flops_a / (avg_a / 1e3) / 1e12, 2),
                      "fp64_frac": round(flops_a / (avg_a / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 4),

@@ -168,12 +168,16 @@ int ipdg_refop_host(int N, int which, double* host, int64_t cap);
 int ipdg_get_geofacs(ipdg_ctx ctx, double* host, int64_t cap);
 /* K*3 neighbour element (-1 boundary) and K*3 neighbour face */
 int ipdg_get_connectivity(ipdg_ctx ctx, int32_t* etoe, int32_t* etof, int64_t cap);
-/* out[0..n): N, Np, K, nblocks, E (own elements per block), Gmax, smem bytes/CTA, grid */
+/* out[0..n), n <= 11: N, Np, K, nblocks, E (own elements per block), Gmax, smem bytes/CTA and grid of
+ * k_sipdg, then the pass-A kernel the context resolves to for lambda = 0 (1 k_sipdg, 2 k_grad + k_flux,
+ * 3 k_tpe, 4 k_pipe) with its smem bytes/CTA and grid */
 int ipdg_info(ipdg_ctx ctx, int64_t* out, int n);
-/* Operator kernel variant: 0 auto (the variant measured fastest for the degree), 1 fused
- * single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels (k_grad, k_flux, DMMA),
- * 3 thread-per-element (k_tpe, DFMA with operators in constant memory; N <= 4 only, else
- * IPDG_EINVAL).  Results agree to rounding.  Switching drops captured CG graphs. */
+/* Operator kernel variant: 0 auto (the variant measured fastest for the degree: 3 for N <= 2, 4 for
+ * N = 3..5, 2 for N >= 6), 1 fused single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels
+ * (k_grad, k_flux, DMMA), 3 thread-per-element (k_tpe, DFMA with operators in constant memory; N <= 4
+ * only, else IPDG_EINVAL), 4 software-pipelined fused (k_pipe, DMMA, TMA-staged rows; falls back to 1
+ * when an operand is not 16-byte aligned or the block does not fit in shared memory).  Results agree
+ * to rounding.  Switching drops captured CG graphs. */
 int ipdg_set_variant(ipdg_ctx ctx, int variant);
 /* number of kernel launches this context has issued (evidence counter) */
 int64_t ipdg_launch_count(ipdg_ctx ctx);

@@ -222,13 +222,14 @@ class Ipdg:
         return e.reshape(self.K, 3), f.reshape(self.K, 3)
 
     def info(self):
-        out = (ctypes.c_int64 * 8)()
-        check(lib().ipdg_info(self.ctx, out, 8), self.ctx)
-        keys = ["N", "Np", "K", "nblocks", "E", "gmax", "smem_bytes", "grid"]
+        out = (ctypes.c_int64 * 11)()
+        check(lib().ipdg_info(self.ctx, out, 11), self.ctx)
+        keys = ["N", "Np", "K", "nblocks", "E", "gmax", "smem_bytes", "grid", "kernel", "kernel_smem_bytes", "kernel_grid"]
         return dict(zip(keys, list(out)))
 
     def set_variant(self, variant):
-        """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux)."""
+        """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux), 3 thread-per-element (k_tpe, N <= 4),
+        4 pipelined fused (k_pipe)."""
         check(lib().ipdg_set_variant(self.ctx, int(variant)), self.ctx)
 
     def launch_count(self):

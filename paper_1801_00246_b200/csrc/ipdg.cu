@@ -457,14 +457,19 @@ struct Impl {
     }
   }
 
-  // auto (variant 0): thread-per-element for N <= 3, fused for N = 4, 5, split for N >= 6 -- the
-  // fastest per degree on C3 (profiles/r01_sweep_variants_tpe.jsonl)
-  static bool use_tpe(ipdg_ctx c) { return c->variant == 3 || (c->variant == 0 && N <= 3); }
-  static bool use_split(ipdg_ctx c) { return c->variant == 2 || (c->variant == 0 && N >= 6); }
   // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
-  static bool use_pipe(ipdg_ctx c, int mode, bool lam, const void* v) {
-    return c->variant == 4 && c->grid_pipe[mode][lam] > 0 && aligned16(v);
+  // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe).
+  // Auto (variant 0): thread-per-element for N <= 2, pipelined fused for N = 3..5, split for N >= 6 --
+  // the fastest per degree on C3 Ax and on the C2 (N = 4) / C4 (N = 6) PCG steps
+  // (profiles/r01_sweep_pipe.jsonl, profiles/r01_bench_*.json).
+  // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
+  static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
+    int k = c->variant;
+    if (k == 0) k = (N <= 2) ? 3 : (N <= 5 ? 4 : 2);
+    if (k == 3 && N > 4) k = 1;
+    if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
+    return k;
   }
 
   static SplitArgs sargs(ipdg_ctx c) {
@@ -545,14 +550,15 @@ struct Impl {
   }
 
   static int ax(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
-    if (use_tpe(c)) return ax_tpe(c, u, Au, lambda, s);
-    if (use_split(c)) return ax_split(c, u, Au, lambda, s);
+    const bool lam = lambda != 0.0;
+    const int k = resolve(c, 0, lam, u);
+    if (k == 3) return ax_tpe(c, u, Au, lambda, s);
+    if (k == 2) return ax_split(c, u, Au, lambda, s);
     AxArgs a = args(c);
     a.u = u;
     a.Au = Au;
     a.lambda = lambda;
-    const bool lam = lambda != 0.0;
-    if (use_pipe(c, 0, lam, u)) {
+    if (k == 4) {
       const int gp = c->grid_pipe[0][lam];
       if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
       else k_pipe<N, MODE_AX, false><<<gp, T::W * 32, c->smem_pipe[0][0], s>>>(a, c->gmax);
@@ -569,8 +575,9 @@ struct Impl {
   }
 
   static int pass_a(ipdg_ctx c, cudaStream_t s) {
-    if (use_tpe(c)) return pass_a_tpe(c, s);
-    if (use_split(c)) return pass_a_split(c, s);
+    const int k = resolve(c, 1, c->lambda != 0.0, c->x);
+    if (k == 3) return pass_a_tpe(c, s);
+    if (k == 2) return pass_a_split(c, s);
     AxArgs a = args(c);
     a.lambda = c->lambda;
     a.r = c->r;
@@ -585,7 +592,7 @@ struct Impl {
     a.partials = c->partials;
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
-    if (use_pipe(c, 1, lam, c->x)) {
+    if (k == 4) {
       const int gp = c->grid_pipe[1][lam];
       if (lam) k_pipe<N, MODE_PCG_A, true><<<gp, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
       else k_pipe<N, MODE_PCG_A, false><<<gp, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
@@ -1537,8 +1544,17 @@ int ipdg_get_connectivity(ipdg_ctx c, int32_t* etoe, int32_t* etof, int64_t cap)
 
 int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   if (!c || !out) return IPDG_EINVAL;
-  const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0]};
-  for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+  // resolved pass-A kernel for lambda = 0 and its launch shape
+  const int kern = [&]() -> int { switch (c->N) {
+      case 1: return Impl<1>::resolve(c, 1, false, nullptr); case 2: return Impl<2>::resolve(c, 1, false, nullptr);
+      case 3: return Impl<3>::resolve(c, 1, false, nullptr); case 4: return Impl<4>::resolve(c, 1, false, nullptr);
+      case 5: return Impl<5>::resolve(c, 1, false, nullptr); case 6: return Impl<6>::resolve(c, 1, false, nullptr);
+      case 7: return Impl<7>::resolve(c, 1, false, nullptr); default: return Impl<8>::resolve(c, 1, false, nullptr); } }();
+  const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : (int64_t)c->smem[1][0];
+  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : c->grid[1][0];
+  const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0],
+                       kern, ksm, kgr};
+  for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
   return IPDG_OK;
 }
 

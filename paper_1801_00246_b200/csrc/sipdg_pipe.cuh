@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
   constexpr int NP = T::NP, NFP = T::NFP, NT = T::NT, TS = P::TS, GF = P::GF;
   constexpr int W = T::W, E = T::E, KCG = T::KCG, KCW = T::KCW, KCM = T::KCM;
   constexpr int NTHR = W * 32;
+  // bulk-copy issue duty on the last warps, which get no ghost P1 tile while Gb <= 8 (W - 2)
+  constexpr int TMA_T = NTHR - 32, XTMA_T = NTHR - 64;
   constexpr bool PCG = (MODE == MODE_PCG_A);
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32 * 3];
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
   }
 
   // ---- issue the loads of one block into staging buffer `sb`: every copy registers its bytes on
-  // mbar (no arrival); thread 0 arrives once all threads have issued (after the next block barrier)
+  // mbar (no arrival); thread TMA_T arrives once all threads have issued (after the next block barrier)
   auto issue = [&](double* sb, const int* mt, const int* gl, int& shift, bool& tma) {
     constexpr int GSTR = P::GSTR;
     const int64_t e0 = mt[0];
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     const int64_t gbase = g0 - shift;
     const unsigned nbytes = (unsigned)(((Eb * NP + shift) * 8 + 15) & ~15);
     tma = (gbase + nbytes / 8 <= K * NP);
-    if (tid == 0) {
+    if (tid == TMA_T) {
       const unsigned rec = (unsigned)Eb * 32u + (unsigned)Eb * 96u;
       mbar_add_tx(mbar, rec + (tma ? nbytes * (1u + (with_p ? 1u : 0u)) : 0u));
       tma_load_1d(gG, a.gG + e0, (unsigned)Eb * 32u, mbar);
@@ -298,12 +300,12 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     const unsigned nbytes = (unsigned)(((Eb * NP + shift) * 8 + 15) & ~15);
     double* xs = sm + L.xs;
     if (gbase + nbytes / 8 <= K * NP) {
-      if (tid == 0) {
+      if (tid == XTMA_T) {
         mbar_expect_tx(mbar + 1, nbytes);
         tma_load_1d(xs, a.x + gbase, nbytes, mbar + 1);
       }
     } else {
-      if (tid == 0) mbar_expect_tx(mbar + 1, 0u);
+      if (tid == XTMA_T) mbar_expect_tx(mbar + 1, 0u);
       for (int q = tid; q < Eb * NP; q += NTHR) cp_async8(xs + q, a.x + g0 + q);
     }
   };
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     issue(sm + L.stg, meta, gids0, cur_shift, cur_tma);
     if (with_x) issue_x(meta);
     __syncthreads();  // every thread has registered its copies
-    if (tid == 0) mbar_arrive(mbar);
+    if (tid == TMA_T) mbar_arrive(mbar);
     const int b1 = blockIdx.x + G;
     if (b1 < a.nblocks) {  // ghost ids of block 1 -> gids[1]
       const int g0 = meta[4 + 2], g1 = meta[4 + 3];
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     PHASE_MARK(3);  // P1 + volume DMMAs (warp 0)
     __syncthreads();  // traces of every slot written; x rows of this block consumed
     PHASE_MARK(4);  // barrier
-    if (tid == 0 && b + G < a.nblocks) mbar_arrive(mbar);  // block b + G: every copy is registered
+    if (tid == TMA_T && b + G < a.nblocks) mbar_arrive(mbar);  // block b + G: every copy is registered
     if (with_x && b + G < a.nblocks) issue_x(meta + 4 * ((it + 1) & 3));
 
     // ---- P2 + P3 face part per warp on its own tile
