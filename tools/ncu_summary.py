@@ -28,7 +28,7 @@ KEYS = {
     "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "l2_bytes": "lts__t_bytes.sum",
 }
-SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1.0, "ms": 1e3, "ns": 1e-3}
+SCALE = {"Kbyte/block": 1e3, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1.0, "ms": 1e3, "ns": 1e-3}
 
 
 def main():
@@ -55,6 +55,10 @@ def main():
                 d[k] = v
         if "dram_read_bytes" in d and "dram_write_bytes" in d:
             d["dram_bytes"] = d["dram_read_bytes"] + d["dram_write_bytes"]
+        st = {h.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(r[j].replace(",", "") or 0)
+              for h, j in idx.items() if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")}
+        tot = sum(st.values()) or 1.0
+        d["stall_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:8]}
         out.append(d)
     json.dump({"source": os.path.basename(a.rep), "N": a.N, "K": a.K, "launches": out}, open(a.out + ".json", "w"), indent=1)
     with open(a.out + ".md", "w") as f:
@@ -64,15 +68,20 @@ def main():
                 d["id"], d["kernel"][:40], d.get("duration_us", 0), d.get("dram_bytes", 0) / 1e6, d.get("dmma_pipe_pct", 0),
                 d.get("fp64_pipe_pct", 0), d.get("smem_pct", 0), d.get("smem_bank_conflicts", 0), d.get("ipc", 0),
                 int(d.get("registers", 0)), d.get("dyn_smem_bytes", 0) / 1e3))
-    pa = [d for d in out if "k_sipdg<%d, 1" % a.N in d["kernel"]]
+        f.write("\nWarp-state samples (% of all samples):\n\n")
+        for d in out:
+            f.write("- %s %s: %s\n" % (d["id"], d["kernel"][:40], ", ".join("%s %.1f" % kv for kv in d["stall_pct"].items())))
+    def kname(d):
+        return d["kernel"].split("<")[0].split()[-1].split("::")[-1]
+    pa = [d for d in out if ("<%d, 1" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe")]
     summ_path = os.path.join(os.path.dirname(a.out), "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     if pa:
-        summ["pass_a"] = {"N": a.N, "K": a.K, "dram_bytes_per_launch": pa[0].get("dram_bytes"),
+        summ["pass_a"] = {"N": a.N, "K": a.K, "kernel": kname(pa[0]), "dram_bytes_per_launch": pa[0].get("dram_bytes"),
                           "duration_us_under_ncu": pa[0].get("duration_us"), "source": os.path.basename(a.rep)}
-    ax = [d for d in out if "k_sipdg<%d, 0" % a.N in d["kernel"]]
+    ax = [d for d in out if ("<%d, 0" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe")]
     if ax:
-        summ["ax"] = {"N": a.N, "K": a.K, "dram_bytes_per_launch": ax[0].get("dram_bytes"),
+        summ["ax"] = {"N": a.N, "K": a.K, "kernel": kname(ax[0]), "dram_bytes_per_launch": ax[0].get("dram_bytes"),
                       "duration_us_under_ncu": ax[0].get("duration_us"), "source": os.path.basename(a.rep)}
     json.dump(summ, open(summ_path, "w"), indent=1)
     print(open(a.out + ".md").read())
