@@ -66,3 +66,44 @@ def test_jacobi_is_symmetric_and_helps():
     _, s1 = solvers.pcg(lambda v: A @ v, b, 1e-8, 5000, dinv=1.0 / A.diagonal())
     assert s0["status"] == s1["status"] == solvers.OK
     assert s1["iterations"] < s0["iterations"]
+
+
+@pytest.mark.parametrize("N", [1, 3, 5])
+def test_inverse_mass_preconditioner_inverts_the_assembled_mass_part(N):
+    """P:221 block-Jacobi: the preconditioner is the exact inverse of lambda * blockdiag(J^e M), checked
+    against the quadrature assembly (A(lambda) - A(0) = lambda * mass), and it is symmetric."""
+    m = meshgen.square(5, jitter=0.2, diag="random", order="morton", seed=4)
+    ref = RefElem(N)
+    lam = 7.0
+    Ml = (assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+          - assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=0.0))
+    P = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam)
+    rng = np.random.default_rng(5)
+    v, w = rng.uniform(-1, 1, (2, Ml.shape[0]))
+    assert np.linalg.norm(P(Ml @ v) - v) <= 1e-12 * np.linalg.norm(v)
+    assert abs(w @ P(v) - v @ P(w)) <= 1e-12 * abs(w @ P(v))
+    with pytest.raises(ValueError):
+        solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, 0.0)
+
+
+def test_block_jacobi_effective_for_mass_dominated_screened_poisson():
+    """for small time steps the screened operator is dominated by the mass term, so the scaled
+    inverse mass is an effective preconditioner (few iterations at large lambda = 1/(nu dt), fewer than
+    point Jacobi), and its iteration count grows as the time step grows (smaller lambda); the solution
+    matches a direct solve."""
+    m = meshgen.square(6, jitter=0.2, diag="random", order="morton", seed=8)
+    ref = RefElem(3)
+    its = []
+    for lam, cap in ((1e8, 4), (1e6, 8), (1e4, None), (1e2, None)):
+        A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref, lam=lam)
+        b = np.random.default_rng(9).uniform(-1, 1, A.shape[0])
+        P = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam)
+        x, st = solvers.pcg(lambda v: A @ v, b, 1e-10, 1000, apply_P=P)
+        assert st["status"] == solvers.OK
+        its.append(st["iterations"])
+        if cap is not None:
+            _, sj = solvers.pcg(lambda v: A @ v, b, 1e-10, 1000, dinv=1.0 / A.diagonal())
+            assert st["iterations"] <= cap and st["iterations"] < sj["iterations"]
+        xd = spla.spsolve(A.tocsc(), b)
+        assert np.linalg.norm(x - xd) <= 1e-7 * np.linalg.norm(xd)
+    assert its == sorted(its)
