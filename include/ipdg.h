@@ -54,6 +54,8 @@ extern "C" {
 /* preconditioners for ipdg_pcg_* */
 #define IPDG_PRECOND_NONE 0
 #define IPDG_PRECOND_JACOBI 1 /* point Jacobi D = diag(A) (R11) */
+#define IPDG_PRECOND_BLOCK_JACOBI 2 /* screened Poisson (lambda > 0, else IPDG_EINVAL): the scaled inverse
+                                     * mass matrix on each element, (lambda J^e M)^{-1} */
 
 typedef struct ipdg_ctx_s* ipdg_ctx;
 
@@ -98,7 +100,7 @@ int ipdg_nodes(ipdg_ctx ctx, double* x, double* y, void* stream);
 int ipdg_workspace_bytes(ipdg_ctx ctx, int64_t* bytes);
 int ipdg_set_workspace(ipdg_ctx ctx, void* dev, int64_t bytes);
 
-/* Solve A x = b by (Jacobi-)PCG (R12): x in = x0, out = solution.
+/* Solve A x = b by PCG (R12), precond = IPDG_PRECOND_*: x in = x0, out = solution.
  * Stops when ||r_k||_2 <= tol ||b||_2 or after maxit iterations (IPDG_NOT_CONVERGED).
  * b = 0 returns x = 0 with 0 iterations.  Blocks until the result is known; the
  * iteration loop runs on the device (no host sync per iteration). */

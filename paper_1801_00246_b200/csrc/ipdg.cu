@@ -34,6 +34,7 @@
 #include "sipdg_split.cuh"
 #include "sipdg_tpe.cuh"
 #include "sipdg_pipe.cuh"
+#include "pcg_blockjacobi.cuh"
 
 using namespace ipdg;
 
@@ -56,6 +57,7 @@ struct ipdg_ctx_s {
   double* vxy = nullptr;
   double* rs = nullptr;
   double* Mref = nullptr;
+  double* Minv = nullptr;  // M^{-1} (block-Jacobi preconditioner)
   double* tables = nullptr;
   double* diagtab = nullptr;
   int nblocks = 0, gmax = 0;
@@ -67,6 +69,7 @@ struct ipdg_ctx_s {
   // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit
   size_t smem_pipe[2][2] = {{0, 0}, {0, 0}};
   int grid_pipe[2][2] = {{0, 0}, {0, 0}};
+  bool pipe_xb[2] = {false, false};  // [lam]: k_pipe's pass A leaves x to pass B (no room for x staging)
   // thread-per-element variant (k_tpe): its own block schedule
   int t_nblocks = 0;
   int *t_boff = nullptr, *t_goff = nullptr, *t_gid = nullptr;
@@ -340,17 +343,27 @@ struct Impl {
   static int configure_pipe(ipdg_ctx c, int optin) {
     for (int lam = 0; lam < 2; ++lam)
       for (int mode = 0; mode < 2; ++mode) {
-        const PipeLayout L = PipeLayout::make<N>(c->gmax, lam != 0, mode == 1);
-        const size_t bytes = (size_t)L.total() * sizeof(double);
-        c->smem_pipe[mode][lam] = bytes;
-        c->grid_pipe[mode][lam] = 0;
-        if ((int)bytes > optin - 1024) continue;
         const void* fn = (mode == 0) ? (lam ? (const void*)k_pipe<N, MODE_AX, true> : (const void*)k_pipe<N, MODE_AX, false>)
                                      : (lam ? (const void*)k_pipe<N, MODE_PCG_A, true> : (const void*)k_pipe<N, MODE_PCG_A, false>);
-        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        int occ = 0;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
-        if (occ >= 1) c->grid_pipe[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
+        c->grid_pipe[mode][lam] = 0;
+        c->pipe_xb[lam] = false;
+        int best = 0;
+        // PCG pass A: stage x for the deferred update unless that costs a resident CTA per SM, in which
+        // case pass B updates x (AxArgs::defer_x = 0)
+        for (int xs = 1; xs >= (mode == 1 ? 0 : 1); --xs) {
+          const PipeLayout L = PipeLayout::make<N>(c->gmax, lam != 0, mode == 1, xs != 0);
+          const size_t bytes = (size_t)L.total() * sizeof(double);
+          if ((int)bytes > optin - 1024) continue;
+          CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+          int occ = 0;
+          CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
+          if (occ > best) {
+            best = occ;
+            c->smem_pipe[mode][lam] = bytes;
+            c->grid_pipe[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
+            if (mode == 1) c->pipe_xb[lam] = (xs == 0);
+          }
+        }
       }
     return IPDG_OK;
   }
@@ -608,6 +621,21 @@ struct Impl {
     return IPDG_OK;
   }
 
+  // block-Jacobi (scaled inverse mass) residual pass: init (r = b - Ax0) or update (r -= alpha Ap)
+  static int pass_b_bj(ipdg_ctx c, bool init, const double* b, cudaStream_t s) {
+    constexpr int EPB = 256 / T::NP;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->K + EPB - 1) / EPB, (int64_t)c->sms * 8));
+    if (init)
+      k_pcg_bj<N, true><<<grid, 256, 0, s>>>(c->K, b, c->Ap, c->r, c->zb, c->gG, c->Minv, c->lambda, c->st, c->partials,
+                                             c->counter, nullptr, nullptr, nullptr);
+    else
+      k_pcg_bj<N, false><<<grid, 256, 0, s>>>(c->K, c->r, c->Ap, c->r, c->zb, c->gG, c->Minv, c->lambda, c->st,
+                                              c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
   static int diag(ipdg_ctx c, double* d, double lambda, cudaStream_t s) {
     const int64_t n = c->K * T::NP;
     k_diag<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->etoe, c->bcode, c->diagtab, c->tau_c, lambda, d);
@@ -807,7 +835,7 @@ int ipdg_destroy(ipdg_ctx c) {
   cudaSetDevice(c->device);
   free_mesh(c);
   free_ws(c);
-  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->st, c->counter, c->partials};
+  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->Minv, c->st, c->counter, c->partials};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
@@ -1249,14 +1277,20 @@ static int halo_for_p(ipdg_ctx c, cudaStream_t s) {
   return halo_exchange(c, s);
 }
 
-static int one_iteration(ipdg_ctx c, cudaStream_t s) {
-  TRY(halo_for_p(c, s));
-  TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
-  TRY(allreduce(c, &c->st->red_A, 1, s));
+static int pass_b(ipdg_ctx c, cudaStream_t s) {
+  if (c->precond == IPDG_PRECOND_BLOCK_JACOBI) DISPATCH(c->N, pass_b_bj(c, false, nullptr, s));
   k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
                                         c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+static int one_iteration(ipdg_ctx c, cudaStream_t s) {
+  TRY(halo_for_p(c, s));
+  TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
+  TRY(allreduce(c, &c->st->red_A, 1, s));
+  TRY(pass_b(c, s));
   TRY(allreduce(c, c->st->red_B, 2, s));
   return IPDG_OK;
 }
@@ -1279,7 +1313,9 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
 }
 
 int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, void* stream) {
-  if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || (precond != 0 && precond != 1)) return IPDG_EINVAL;
+  if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || precond < 0 || precond > 2) return IPDG_EINVAL;
+  if (precond == IPDG_PRECOND_BLOCK_JACOBI && !(lambda > 0.0))
+    FAIL(c, IPDG_EINVAL, "block-Jacobi (scaled inverse mass) preconditioning needs lambda > 0");
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
   const bool dir = (c->H > 0 || c->S > 0) ? c->has_dirichlet_global : c->has_dirichlet;
   if (lambda == 0.0 && !dir) FAIL(c, IPDG_ESINGULAR, "lambda = 0 and no Dirichlet face");
@@ -1287,7 +1323,10 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   TRY(ensure_ws(c));
   TRY(ensure_partials(c));
   const int64_t n = c->K * c->ref.Np;
-  if (precond && !(c->dinv_valid && c->dinv_lambda == lambda)) {
+  if (precond == IPDG_PRECOND_BLOCK_JACOBI && !c->Minv) {
+    TRY(upload(c, &c->Minv, c->ref.Minv.data(), c->ref.Minv.size()));
+  }
+  if (precond == IPDG_PRECOND_JACOBI && !(c->dinv_valid && c->dinv_lambda == lambda)) {
     TRY(ipdg_diag(c, c->dinv, lambda, stream));
     k_recip<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, c->dinv);
     c->launches++;
@@ -1297,9 +1336,15 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   c->x = x;
   c->lambda = lambda;
   c->precond = precond;
-  // x is updated by pass A (deferred x += alpha_{k-1} p_{k-1}).  The alternative protocol, x += alpha_k p_k
-  // in pass B (k_pcg_b with x), measured slower on C2 with k_pipe (pass B 18 -> 29 us, pass A -3 us).
-  c->xb = false;
+  // x is updated by pass A (deferred x += alpha_{k-1} p_{k-1}) -- measured faster on C2 than x += alpha_k p_k
+  // in pass B (pass B 18 -> 29 us, pass A -3 us) -- unless k_pipe would lose a resident CTA per SM to the
+  // x staging buffer (e.g. the lambda variant at N = 4), then pass B updates x.
+  c->xb = [&]() -> bool { switch (c->N) {
+      case 1: return Impl<1>::resolve(c, 1, lambda != 0.0, x) == 4; case 2: return Impl<2>::resolve(c, 1, lambda != 0.0, x) == 4;
+      case 3: return Impl<3>::resolve(c, 1, lambda != 0.0, x) == 4; case 4: return Impl<4>::resolve(c, 1, lambda != 0.0, x) == 4;
+      case 5: return Impl<5>::resolve(c, 1, lambda != 0.0, x) == 4; case 6: return Impl<6>::resolve(c, 1, lambda != 0.0, x) == 4;
+      case 7: return Impl<7>::resolve(c, 1, lambda != 0.0, x) == 4; default: return Impl<8>::resolve(c, 1, lambda != 0.0, x) == 4; } }()
+           && c->pipe_xb[lambda != 0.0];
   PcgState h;
   std::memset(&h, 0, sizeof(h));
   h.tol2 = tol * tol;
@@ -1309,10 +1354,14 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   *c->st_host = h;
   CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
   TRY(ipdg_ax(c, x, c->Ap, lambda, stream));
-  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->zb, c->st, c->partials,
-                                         c->counter);
-  c->launches++;
-  CUDA_TRY(c, cudaGetLastError());
+  if (precond == IPDG_PRECOND_BLOCK_JACOBI) {
+    TRY([&]() -> int { DISPATCH(c->N, pass_b_bj(c, true, b, s)); }());
+  } else {
+    k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->zb, c->st, c->partials,
+                                           c->counter);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+  }
   TRY(allreduce(c, c->st->red_B, 3, s));
   // (re)capture the iteration graphs when the operands changed
   if (c->gkey_x != (const void*)x || c->gkey_lambda != lambda || c->gkey_precond != precond || !c->gexec[0]) {
@@ -1367,10 +1416,7 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b,
       if (rc != IPDG_OK) break;
       if ((rc = allreduce(c, &c->st->red_A, 1, s)) != IPDG_OK) break;
       cudaEventRecord(ev[3 * i + 1], s);
-      k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
-                                            c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe,
-                                            c->po);
-      c->launches++;
+      if ((rc = pass_b(c, s)) != IPDG_OK) break;
       cudaEventRecord(ev[3 * i + 2], s);
       if ((rc = allreduce(c, c->st->red_B, 2, s)) != IPDG_OK) break;
     }

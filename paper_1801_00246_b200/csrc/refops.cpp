@@ -219,6 +219,7 @@ RefOps build_refops(int N) {
       for (int b = 0; b < Nfp; ++b) E[R.Fmask[f * Nfp + a] * 3 * Nfp + f * Nfp + b] = R.M1D[a * Nfp + b];
   const std::vector<double> VVt = matmul(V, transpose(V, Np, Np), Np, Np, Np);
   R.LIFT = matmul(VVt, E, Np, Np, 3 * Nfp);
+  R.Minv = VVt;
   R.Sr = matmul(R.M, R.Dr, Np, Np, Np);
   R.Ss = matmul(R.M, R.Ds, Np, Np, Np);
   return R;

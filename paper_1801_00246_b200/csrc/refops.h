@@ -13,6 +13,7 @@ struct RefOps {
   std::vector<double> Sr, Ss;        // M Dr, M Ds
   std::vector<double> M1D;           // Nfp x Nfp face mass on [-1,1]
   std::vector<double> LIFT;          // Np x 3Nfp, M^{-1} E (Eq. elLift)
+  std::vector<double> Minv;          // Np x Np, M^{-1} = V V^T (block-Jacobi preconditioner)
   std::vector<int> Fmask;            // 3 x Nfp node ids of each face
 };
 

@@ -37,7 +37,8 @@ struct PipeLayout {
   int tabG, tabM, tabL, iaux, meta, trc, gid, mbar, xs, stg, sz;
   int o_u0, o_u1, o_g0, o_g1, o_gG, o_gF, o_nb, o_gs;  // within one staging buffer
   template <int N>
-  __host__ __device__ static PipeLayout make(int gmax, bool lam, bool pcg) {
+  // xs: PCG pass A stages x for the deferred update (else pass B updates x, see AxArgs::defer_x)
+  __host__ __device__ static PipeLayout make(int gmax, bool lam, bool pcg, bool xs = true) {
     using T = Tr<N>;
     using P = TrPipe<N>;
     PipeLayout L;
@@ -54,7 +55,7 @@ struct PipeLayout {
     L.gid = o; o += gm8;                      // 2 x gm8 ints
     o = (o + 1) & ~1;
     L.mbar = o; o += 2;
-    L.xs = o; o += pcg ? P::OSTR : 0;        // own rows of x for the deferred update (single buffer)
+    L.xs = o; o += (pcg && xs) ? P::OSTR : 0;  // own rows of x for the deferred update (single buffer)
     // one staging buffer (two of them): own rows | p_{k-1} own | ghost rows | p_{k-1} ghosts |
     // J G^T G + J per slot | face records (own) | neighbour slots (own)
     int q = 0;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
   constexpr bool PCG = (MODE == MODE_PCG_A);
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32 * 3];
-  const PipeLayout L = PipeLayout::make<N>(gmax, LAM, PCG);
+  const PipeLayout L = PipeLayout::make<N>(gmax, LAM, PCG, a.defer_x != 0);
   const int gm8 = (gmax + 7) / 8 * 8;
   double* tabG = sm + L.tabG;
   double* tabM = sm + L.tabM;

@@ -23,8 +23,9 @@ def check_solve(m, N, precond, tol, lam=0.0, maxit=20000, f=meshgen.sin_sin_forc
     op = Ipdg(N, m)
     op.set_variant(variant)
     x, st = op.pcg_solve(gpu(b), lam=lam, precond=precond, tol=tol, maxit=maxit)
-    dinv = 1.0 / A.diagonal() if precond else None
-    xo, sto = solvers.pcg(lambda v: A @ v, b.ravel(), tol, maxit, dinv=dinv)
+    dinv = 1.0 / A.diagonal() if precond == 1 else None
+    P = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam) if precond == 2 else None
+    xo, sto = solvers.pcg(lambda v: A @ v, b.ravel(), tol, maxit, dinv=dinv, apply_P=P)
     assert st["status"] == sto["status"] == 0
     # +-1 iteration (north star); on solves of several hundred iterations the rounding-order
     # differences (FMA contraction, DMMA accumulation, reduction trees) may move the count by up to
@@ -120,3 +121,21 @@ def test_split_api_matches_solve_and_host_path():
     xh = torch.zeros_like(bh).pin_memory()
     st3 = op.pcg_solve_host(bh, xh, precond=1, tol=1e-9, maxit=1000)
     assert st3["iterations"] == st1["iterations"] and torch.equal(xh, x1.cpu())
+
+
+@pytest.mark.parametrize("N", [1, 3, 4, 6, 8])
+@pytest.mark.parametrize("lam", [1e6, 1e3])
+def test_block_jacobi_screened_poisson(N, lam):
+    """screened Poisson -L + lambda with the scaled inverse mass preconditioner,
+    against the oracle PCG with the same preconditioner (iterations, residual)."""
+    m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=21,
+                       tag=lambda x, y: np.where(y < 0.5, 1, 2).astype(np.int8))
+    check_solve(m, N, 2, 1e-10, lam=lam)
+
+
+def test_block_jacobi_needs_positive_lambda():
+    m = meshgen.square(4)
+    op = Ipdg(2, m)
+    b = torch.ones(op.K, op.Np, dtype=torch.float64, device="cuda")
+    with pytest.raises(IpdgError):
+        op.pcg_solve(b, precond=2, lam=0.0)
