@@ -39,7 +39,7 @@ def peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-KERNEL_NAMES = {1: "k_sipdg", 2: "k_grad+k_flux", 3: "k_tpe", 4: "k_pipe"}
+KERNEL_NAMES = {1: "k_sipdg", 2: "k_grad+k_flux", 3: "k_tpe", 4: "k_pipe", 5: "k_gather"}
 FP64_PEAK_TFLOPS = 36.8  # measured DFMA / DMMA peak on this pool's B200 (profiles/r01_micro_fp64.jsonl)
 
 
@@ -424,7 +424,7 @@ def run_sweep(args):
     nx = args.sweep_nx
     mesh = meshgen.square(nx, jitter=0.2, diag="random", order="morton", seed=3)
     stream = torch.cuda.current_stream()
-    for N, variant in [(N, v) for N in range(1, 9) for v in args.sweep_variants if v != 3 or N <= 4]:
+    for N, variant in [(N, v) for N in range(1, 9) for v in args.sweep_variants if v not in (3, 5) or N <= 4]:
         op = Ipdg(N, mesh)
         op.set_variant(variant)
         K, Np = op.K, op.Np

@@ -172,14 +172,15 @@ int ipdg_get_geofacs(ipdg_ctx ctx, double* host, int64_t cap);
 int ipdg_get_connectivity(ipdg_ctx ctx, int32_t* etoe, int32_t* etof, int64_t cap);
 /* out[0..n), n <= 11: N, Np, K, nblocks, E (own elements per block), Gmax, smem bytes/CTA and grid of
  * k_sipdg, then the pass-A kernel the context resolves to for lambda = 0 (1 k_sipdg, 2 k_grad + k_flux,
- * 3 k_tpe, 4 k_pipe) with its smem bytes/CTA and grid */
+ * 3 k_tpe, 4 k_pipe, 5 k_gather) with its smem bytes/CTA and grid */
 int ipdg_info(ipdg_ctx ctx, int64_t* out, int n);
-/* Operator kernel variant: 0 auto (the variant measured fastest for the degree: 3 for N <= 2, 4 for
+/* Operator kernel variant: 0 auto (the variant measured fastest for the degree: 5 for N <= 2, 4 for
  * N = 3..5, 2 for N >= 6), 1 fused single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels
- * (k_grad, k_flux, DMMA), 3 thread-per-element (k_tpe, DFMA with operators in constant memory; N <= 4
- * only, else IPDG_EINVAL), 4 software-pipelined fused (k_pipe, DMMA, TMA-staged rows; falls back to 1
- * when an operand is not 16-byte aligned or the block does not fit in shared memory).  Results agree
- * to rounding.  Switching drops captured CG graphs. */
+ * (k_grad, k_flux, DMMA), 3 thread-per-element with block staging (k_tpe, DFMA with operators in
+ * constant memory), 4 software-pipelined fused (k_pipe, DMMA, TMA-staged rows; falls back to 1 when an
+ * operand is not 16-byte aligned or the block does not fit in shared memory), 5 gather (k_gather, one
+ * thread per element reading its neighbours' rows from L1/L2, DFMA).  Variants 3 and 5 need N <= 4
+ * (else IPDG_EINVAL).  Results agree to rounding.  Switching drops captured CG graphs. */
 int ipdg_set_variant(ipdg_ctx ctx, int variant);
 /* number of kernel launches this context has issued (evidence counter) */
 int64_t ipdg_launch_count(ipdg_ctx ctx);

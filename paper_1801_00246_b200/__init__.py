@@ -229,7 +229,7 @@ class Ipdg:
 
     def set_variant(self, variant):
         """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux), 3 thread-per-element (k_tpe, N <= 4),
-        4 pipelined fused (k_pipe)."""
+        4 pipelined fused (k_pipe), 5 gather (k_gather, N <= 4)."""
         check(lib().ipdg_set_variant(self.ctx, int(variant)), self.ctx)
 
     def launch_count(self):

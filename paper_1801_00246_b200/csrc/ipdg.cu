@@ -35,6 +35,7 @@
 #include "sipdg_tpe.cuh"
 #include "sipdg_pipe.cuh"
 #include "pcg_blockjacobi.cuh"
+#include "sipdg_gather.cuh"
 
 using namespace ipdg;
 
@@ -86,6 +87,7 @@ struct ipdg_ctx_s {
   PcgState* st = nullptr;
   PcgState* st_host = nullptr;
   double* partials = nullptr;
+  int partials_cap = 0;  // slots per reduced quantity
   unsigned int* counter = nullptr;
   void* ws = nullptr;
   int64_t ws_bytes = 0;
@@ -472,17 +474,33 @@ struct Impl {
 
   // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
-  // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe).
-  // Auto (variant 0): thread-per-element for N <= 2, pipelined fused for N = 3..5, split for N >= 6 --
+  // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe, 5 gather).
+  // Auto (variant 0): gather for N <= 2, pipelined fused for N = 3..5, split for N >= 6 --
   // the fastest per degree on C3 Ax and on the C2 (N = 4) / C4 (N = 6) PCG steps
   // (profiles/r01_sweep_pipe.jsonl, profiles/r01_bench_*.json).
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N <= 2) ? 3 : (N <= 5 ? 4 : 2);
-    if (k == 3 && N > 4) k = 1;
+    if (k == 0) k = (N <= 2) ? 5 : (N <= 5 ? 4 : 2);
+    if ((k == 3 || k == 5) && N > 4) k = 1;
     if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
     return k;
+  }
+
+  // gather variant (N <= 4): one thread per element, grid-stride
+  template <int MODE>
+  static int launch_gather(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s) {
+    if constexpr (N <= 4) {
+      const int grid = (int)std::max<int64_t>(1, (c->K + 255) / 256);  // one element per thread
+      if (MODE == MODE_PCG_A && grid > c->partials_cap) FAIL(c, IPDG_ECUDA, "partials buffer too small");
+      if (lam) k_gather<N, MODE, true><<<grid, 256, 0, s>>>(a);
+      else k_gather<N, MODE, false><<<grid, 256, 0, s>>>(a);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    } else {
+      FAIL(c, IPDG_EINVAL, "gather variant needs N <= 4");
+    }
   }
 
   static SplitArgs sargs(ipdg_ctx c) {
@@ -557,6 +575,7 @@ struct Impl {
     a.tables = c->tables;
     a.gG = c->gG;
     a.gF = c->gF;
+    a.nbg = c->nbg;
     a.tau_c = c->tau_c;
     a.halo_p = c->halobuf;
     return a;
@@ -571,6 +590,7 @@ struct Impl {
     a.u = u;
     a.Au = Au;
     a.lambda = lambda;
+    if (k == 5) return launch_gather<MODE_AX>(c, a, lam, s);
     if (k == 4) {
       const int gp = c->grid_pipe[0][lam];
       if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
@@ -605,6 +625,7 @@ struct Impl {
     a.partials = c->partials;
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
+    if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
     if (k == 4) {
       const int gp = c->grid_pipe[1][lam];
       if (lam) k_pipe<N, MODE_PCG_A, true><<<gp, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
@@ -1248,8 +1269,12 @@ static int ensure_ws(ipdg_ctx c) {
 }
 
 static int ensure_partials(ipdg_ctx c) {
-  if (c->partials) return IPDG_OK;
-  CUDA_TRY(c, cudaMalloc(&c->partials, 3 * sizeof(double) * std::max(4096, 4 * c->sms * 16)));
+  // one slot per CTA of the largest reducing grid (k_gather: one CTA per 256 elements)
+  const int need = (int)std::max<int64_t>(std::max(4096, 4 * c->sms * 16), (c->K + 255) / 256);
+  if (c->partials && c->partials_cap >= need) return IPDG_OK;
+  if (c->partials) cudaFree(c->partials);
+  CUDA_TRY(c, cudaMalloc(&c->partials, 3 * sizeof(double) * need));
+  c->partials_cap = need;
   return IPDG_OK;
 }
 
@@ -1622,7 +1647,7 @@ int ipdg_debug_phase_cycles(unsigned long long* out8, int reset) {
 }
 
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 4 || (variant == 3 && c->N > 4)) return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 5 || ((variant == 3 || variant == 5) && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

@@ -75,6 +75,7 @@ struct AxArgs {
   const int* boff;       // [nblocks+1] first element of each block
   const double4* geo;    // [K + H] r_x, s_x, r_y, s_y  (H = halo ghosts, multi-GPU)
   const short4* nbr;     // [K] per face: slot (x,y,z), w = flags: face f -> bits 4f..4f+3 = (f' | bc << 2)
+  const int4* nbg;       // [K] neighbour element per face (>= K: halo ghost; self on boundary) + the same flags (k_gather)
   const int* goff;       // [nblocks+1] ghost list offsets
   const int* gid;        // ghost element ids (>= K: halo index K + h)
   const double* tables;  // fragment tables: G | M | L

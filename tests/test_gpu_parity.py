@@ -153,10 +153,11 @@ def test_full_size_c2_parity(N):
     assert err.max() <= 1e-11
 
 
-@pytest.mark.parametrize("N,variant", [(N, v) for N in range(1, 9) for v in (1, 2, 3, 4) if v != 3 or N <= 4])
+@pytest.mark.parametrize("N,variant", [(N, v) for N in range(1, 9) for v in (1, 2, 3, 4, 5) if v not in (3, 5) or N <= 4])
 def test_ax_kernel_variants(N, variant):
     """Fused k_sipdg (variant 1), split k_grad + k_flux (variant 2), thread-per-element k_tpe
-    (variant 3, N <= 4) and the pipelined fused k_pipe (variant 4) all match the oracle."""
+    (variant 3, N <= 4), the pipelined fused k_pipe (variant 4) and the gather kernel k_gather (variant 5,
+    N <= 4) all match the oracle."""
     m = MESHES["mixed_bc"]()
     ref = RefElem(N)
     op = Ipdg(N, m)
@@ -168,7 +169,7 @@ def test_ax_kernel_variants(N, variant):
         assert rel(Au.ravel(), A @ u.ravel()) <= TOL, (N, variant, lam)
 
 
-@pytest.mark.parametrize("N,variant", [(1, 3), (2, 3), (3, 3), (4, 3), (1, 4), (2, 4), (4, 4), (5, 4), (6, 4), (8, 4)])
+@pytest.mark.parametrize("N,variant", [(1, 3), (2, 3), (3, 3), (4, 3), (1, 4), (2, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5)])
 @pytest.mark.parametrize("mesh", ["random_order", "ragged", "tiny"])
 def test_ax_variant_meshes(N, variant, mesh):
     """k_tpe (variant 3) and the pipelined k_pipe (variant 4) on scattered orderings (short blocks at
