@@ -95,6 +95,17 @@ int ipdg_mass(ipdg_ctx ctx, const double* u, double* Mu, void* stream);
 /* Physical node coordinates x, y (device, K*Np each): x = Phi^e(r,s) (Eq. operators1). */
 int ipdg_nodes(ipdg_ctx ctx, double* x, double* y, void* stream);
 
+/* DG gradient and divergence with central fluxes (Eqs. INS_SD_4_1 / INS_SD_4_2):
+ * the nodal operators G p = grad p + 1/2 sum_f (sJ/J) LIFT_f (n [[p]]) and D u = div u + 1/2 sum_f
+ * (sJ/J) LIFT_f (n.[[u]]), i.e. (J^e M)^{-1} times the variational forms of the paper, used for the
+ * pressure right-hand side -(gamma/dt) D.U and the velocity update U - (dt/gamma) G dP (Eq. INS_TD_3).
+ * Homogeneous boundary data by mirroring, with the context's face codes read as PRESSURE types
+ * (R20): IPDG_BC_DIRICHLET (outflow) p+ = -p-, u+ = u-; IPDG_BC_NEUMANN (velocity
+ * Dirichlet) p+ = p-, u+ = -u-.  All fields K x Np device arrays, outputs distinct from inputs;
+ * asynchronous on `stream`.  Single-partition contexts only (IPDG_ESTATE with a halo). */
+int ipdg_dg_grad(ipdg_ctx ctx, const double* p, double* gx, double* gy, void* stream);
+int ipdg_dg_div(ipdg_ctx ctx, const double* ux, const double* uy, double* d, void* stream);
+
 /* Scratch for PCG: query the size, hand over caller-owned device memory (e.g. a torch
  * tensor).  Without ipdg_set_workspace the library allocates it itself on first use. */
 int ipdg_workspace_bytes(ipdg_ctx ctx, int64_t* bytes);

@@ -142,6 +142,20 @@ class Ipdg:
         check(lib().ipdg_ax(self.ctx, _ptr(u), _ptr(out), float(lam), _stream(stream)), self.ctx)
         return out
 
+    def dg_grad(self, p, stream=None):
+        """Nodal DG gradient with central fluxes, G p (Eq. INS_SD_4_1): returns (gx, gy)."""
+        import torch
+        gx, gy = torch.empty_like(p), torch.empty_like(p)
+        check(lib().ipdg_dg_grad(self.ctx, _ptr(p), _ptr(gx), _ptr(gy), _stream(stream)), self.ctx)
+        return gx, gy
+
+    def dg_div(self, ux, uy, stream=None):
+        """Nodal DG divergence with central fluxes, D u (Eq. INS_SD_4_2)."""
+        import torch
+        d = torch.empty_like(ux)
+        check(lib().ipdg_dg_div(self.ctx, _ptr(ux), _ptr(uy), _ptr(d), _stream(stream)), self.ctx)
+        return d
+
     def diag(self, lam=0.0, out=None, stream=None):
         out = self._empty() if out is None else out
         check(lib().ipdg_diag(self.ctx, _ptr(out), float(lam), _stream(stream)), self.ctx)

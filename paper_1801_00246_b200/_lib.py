@@ -39,6 +39,8 @@ SIGNATURES = {
     "ipdg_ax": (_int, [_vp, _vp, _vp, _d, _vp]),
     "ipdg_diag": (_int, [_vp, _vp, _d, _vp]),
     "ipdg_mass": (_int, [_vp, _vp, _vp, _vp]),
+    "ipdg_dg_grad": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "ipdg_dg_div": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "ipdg_nodes": (_int, [_vp, _vp, _vp, _vp]),
     "ipdg_workspace_bytes": (_int, [_vp, _c.POINTER(_i64)]),
     "ipdg_set_workspace": (_int, [_vp, _vp, _i64]),

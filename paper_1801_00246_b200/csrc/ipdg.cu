@@ -36,6 +36,7 @@
 #include "sipdg_pipe.cuh"
 #include "pcg_blockjacobi.cuh"
 #include "sipdg_gather.cuh"
+#include "dgops.cuh"
 
 using namespace ipdg;
 
@@ -59,6 +60,7 @@ struct ipdg_ctx_s {
   double* rs = nullptr;
   double* Mref = nullptr;
   double* Minv = nullptr;  // M^{-1} (block-Jacobi preconditioner)
+  double* dgops = nullptr; // Dr | Ds | LIFT (DG gradient / divergence)
   double* tables = nullptr;
   double* diagtab = nullptr;
   int nblocks = 0, gmax = 0;
@@ -657,6 +659,24 @@ struct Impl {
     return IPDG_OK;
   }
 
+  // DG gradient (div = false: o0, o1 = G p) or divergence (div = true: o0 = D u) with central fluxes
+  static int dgop(ipdg_ctx c, bool div, const double* f0, const double* f1, double* o0, double* o1, cudaStream_t s) {
+    constexpr int EPB = 256 / T::NP;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->K + EPB - 1) / EPB, (int64_t)c->sms * 8));
+    if (div) {
+      constexpr size_t bytes = dgop_smem_doubles<N, true>() * sizeof(double);
+      CUDA_TRY(c, cudaFuncSetAttribute(k_dgop<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      k_dgop<N, true><<<grid, 256, bytes, s>>>(c->K, f0, f1, c->geo, c->nbg, c->dgops, o0, nullptr);
+    } else {
+      constexpr size_t bytes = dgop_smem_doubles<N, false>() * sizeof(double);
+      CUDA_TRY(c, cudaFuncSetAttribute(k_dgop<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      k_dgop<N, false><<<grid, 256, bytes, s>>>(c->K, f0, nullptr, c->geo, c->nbg, c->dgops, o0, o1);
+    }
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
   static int diag(ipdg_ctx c, double* d, double lambda, cudaStream_t s) {
     const int64_t n = c->K * T::NP;
     k_diag<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->etoe, c->bcode, c->diagtab, c->tau_c, lambda, d);
@@ -856,7 +876,7 @@ int ipdg_destroy(ipdg_ctx c) {
   cudaSetDevice(c->device);
   free_mesh(c);
   free_ws(c);
-  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->Minv, c->st, c->counter, c->partials};
+  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->Minv, c->dgops, c->st, c->counter, c->partials};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
@@ -1199,6 +1219,30 @@ int ipdg_ax(ipdg_ctx c, const double* u, double* Au, double lambda, void* stream
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_ax before ipdg_upload_mesh (or ipdg_upload_halo)");
   TRY(halo_for_field(c, u, (cudaStream_t)stream));
   DISPATCH(c->N, ax(c, u, Au, lambda, (cudaStream_t)stream));
+}
+
+static int dgop_check(ipdg_ctx c) {
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "DG gradient/divergence before ipdg_upload_mesh");
+  if (c->H > 0 || c->S > 0) FAIL(c, IPDG_ESTATE, "DG gradient/divergence: partitioned meshes are not supported");
+  if (!c->dgops) {
+    std::vector<double> t(c->ref.Dr);
+    t.insert(t.end(), c->ref.Ds.begin(), c->ref.Ds.end());
+    t.insert(t.end(), c->ref.LIFT.begin(), c->ref.LIFT.end());
+    TRY(upload(c, &c->dgops, t.data(), t.size()));
+  }
+  return IPDG_OK;
+}
+
+int ipdg_dg_grad(ipdg_ctx c, const double* p, double* gx, double* gy, void* stream) {
+  if (!c || !p || !gx || !gy || gx == gy || p == gx || p == gy) return c ? (c->err = "ipdg_dg_grad: bad arguments", IPDG_EINVAL) : IPDG_EINVAL;
+  TRY(dgop_check(c));
+  DISPATCH(c->N, dgop(c, false, p, nullptr, gx, gy, (cudaStream_t)stream));
+}
+
+int ipdg_dg_div(ipdg_ctx c, const double* ux, const double* uy, double* d, void* stream) {
+  if (!c || !ux || !uy || !d || d == ux || d == uy) return c ? (c->err = "ipdg_dg_div: bad arguments", IPDG_EINVAL) : IPDG_EINVAL;
+  TRY(dgop_check(c));
+  DISPATCH(c->N, dgop(c, true, ux, uy, d, nullptr, (cudaStream_t)stream));
 }
 
 int ipdg_diag(ipdg_ctx c, double* d, double lambda, void* stream) {
