@@ -24,7 +24,8 @@ namespace ipdg {
 template <int N>
 struct TrPipe {
   using T = Tr<N>;
-  static constexpr int TS = (T::NF3 + 1) | 1;   // trace row stride (odd: gathers spread over banks); column NF3 = junk
+  static constexpr int TS = (T::NF3 + 4) | 1;   // trace row stride (odd: gathers spread over banks); columns
+                                                 // NF3..NF3+3 = per-lane junk (no write-write races)
   static constexpr int OSTR = T::E * T::NP + 2;  // own staging array stride (TMA head alignment pad)
   static constexpr int GF = 12;                  // per-face record: (c_r, c_s, sJ tau) x 3 faces
   // ghost rows arrive by one bulk copy each of the 16-byte-aligned span around the row: GSTR doubles
@@ -86,10 +87,11 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 }
 
 // trace columns of reference node i (row-by-row node order, refops.cpp): bits 5f..5f+4 = the column
-// f*Nfp + k of the trace row when Fmask[f][k] = i, else the junk column 3 Nfp (branch-free stores)
+// f*Nfp + k of the trace row when Fmask[f][k] = i, else the junk column JUNK (branch-free stores; each of
+// the 4 lanes of an element row has its own junk column)
 template <int N>
-__host__ __device__ inline int node_trace_cols(int i) {
-  constexpr int NFP = N + 1, JUNK = 3 * (N + 1);
+__host__ __device__ inline int node_trace_cols(int i, int JUNK) {
+  constexpr int NFP = N + 1;
   int j = 0, off = 0;
   while (j <= N && off + (N + 1 - j) <= i) { off += N + 1 - j; ++j; }
   if (j > N) return JUNK | (JUNK << 5) | (JUNK << 10);
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
   // (their B rows are zero)
   int tcol[2 * NT];
 #pragma unroll
-  for (int q = 0; q < 2 * NT; ++q) tcol[q] = node_trace_cols<N>(8 * (q >> 1) + 2 * (lane & 3) + (q & 1));
+  for (int q = 0; q < 2 * NT; ++q) tcol[q] = node_trace_cols<N>(8 * (q >> 1) + 2 * (lane & 3) + (q & 1), T::NF3 + (lane & 3));
   int itab[T::NQ];
 #pragma unroll
   for (int q = 0; q < T::NQ; ++q) {

@@ -1,4 +1,5 @@
-"""Small run of every kernel (both variants, Ax + PCG, halo loopback) for compute-sanitizer."""
+"""Small run of every kernel (all variants, Ax + PCG with point and block Jacobi, halo loopback, DG gradient /
+divergence) for compute-sanitizer (memcheck / racecheck / synccheck)."""
 import os
 import sys
 
@@ -10,7 +11,7 @@ from paper_1801_00246_b200 import Ipdg, meshgen, partition  # noqa: E402
 
 m = meshgen.square(6, jitter=0.2, diag="random", order="morton", seed=3, tag=lambda x, y: np.where(x < 0.5, 1, 2).astype(np.int8))
 for N in [int(a) for a in sys.argv[1:]] or [2, 6]:
-    for variant in (1, 2):
+    for variant in [v for v in (1, 2, 3, 4, 5) if v not in (3, 5) or N <= 4]:
         op = Ipdg(N, m)
         op.set_variant(variant)
         u = torch.from_numpy(meshgen.uniform_field(op.K, op.Np, 1)).cuda()
@@ -19,6 +20,9 @@ for N in [int(a) for a in sys.argv[1:]] or [2, 6]:
         op.diag()
         b = op.mass(u)
         op.pcg_solve(b, precond=1, tol=1e-6, maxit=50)
+        op.pcg_solve(b, precond=2, lam=10.0, tol=1e-6, maxit=50)
+        op.dg_grad(u)
+        op.dg_div(u, b)
         part = meshgen.rcb_partition(m["VX"], m["VY"], m["EToV"], 2)
         ranks = partition.split(m, part, 2)
         ops = [Ipdg.from_rank_mesh(N, rm) for rm in ranks]
