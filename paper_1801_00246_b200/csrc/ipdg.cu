@@ -361,6 +361,9 @@ struct Impl {
           CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
           int occ = 0;
           CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
+#ifdef IPDG_EXP_PIPE_ONE_CTA
+          occ = std::min(occ, 1);
+#endif
           if (occ > best) {
             best = occ;
             c->smem_pipe[mode][lam] = bytes;
@@ -1076,7 +1079,7 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   cudaFree(bad);
   if (badh != none) FAIL(c, IPDG_EMESH, "element %llu has J <= 0 (vertices must be counter-clockwise)", badh);
   CUDA_TRY(c, cudaMalloc(&c->gG, KH * sizeof(double4)));
-  CUDA_TRY(c, cudaMalloc(&c->gF, std::max<int64_t>(1, K) * 12 * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->gF, std::max<int64_t>(1, K) * kGF * sizeof(double)));
   k_geofacs<<<(unsigned)((KH + 255) / 256), 256>>>(K, KH, c->geo, c->etoe, c->bcode, c->tau_c, c->gG, c->gF);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());

@@ -80,7 +80,7 @@ struct AxArgs {
   const int* gid;        // ghost element ids (>= K: halo index K + h)
   const double* tables;  // fragment tables: G | M | L
   const double4* gG;     // [K + H] (J G_rr, J G_rs, J G_ss, J) per element (k_pipe)
-  const double* gF;      // [K][12] per face (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau) (k_pipe)
+  const double* gF;      // [K][kGF = 10] per face (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau) (k_pipe, k_gather)
   double tau_c;          // (N+1)(N+2)/2 * tau_scale
   double lambda;
   // MODE_AX

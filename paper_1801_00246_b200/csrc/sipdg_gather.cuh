@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) k_gather(AxArgs a) {
       out[n] = s;
     }
     const int4 nb = a.nbg[e];
-    const double* gf = a.gF + e * 12;
+    const double* gf = a.gF + e * kGF;
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
       const int fl = (nb.w >> (4 * f)) & 15;

@@ -21,13 +21,17 @@
 
 namespace ipdg {
 
+// per-element face record length in doubles: 9 used, padded to 10 so a block's records (80 B each)
+// are a 16-byte multiple for the bulk copy
+constexpr int kGF = 10;
+
 template <int N>
 struct TrPipe {
   using T = Tr<N>;
   static constexpr int TS = (T::NF3 + 4) | 1;   // trace row stride (odd: gathers spread over banks); columns
                                                  // NF3..NF3+3 = per-lane junk (no write-write races)
   static constexpr int OSTR = T::E * T::NP + 2;  // own staging array stride (TMA head alignment pad)
-  static constexpr int GF = 12;                  // per-face record: (c_r, c_s, sJ tau) x 3 faces
+  static constexpr int GF = kGF;                 // per-face record: (c_r, c_s, sJ tau) x 3 faces (+1 pad)
   // ghost rows arrive by one bulk copy each of the 16-byte-aligned span around the row: GSTR doubles
   // (Np + 1 rounded up to even when Np is odd: the row may start on an odd double)
   static constexpr int GSTR = (T::NP & 1) ? T::NP + 1 : T::NP;
@@ -126,7 +130,7 @@ __global__ void k_geofacs(int64_t K, int64_t KH, const double4* __restrict__ geo
       const double4 h = geo[etoe[e * 3 + f]];
       detp = h.x * h.w - h.y * h.z;
     }
-    double* r = gF + e * 12 + 3 * f;
+    double* r = gF + e * kGF + 3 * f;
     r[0] = 0.5 * J * (rx * gx + ry * gy);
     r[1] = 0.5 * J * (sx * gx + sy * gy);
     r[2] = tau_c * (J * J * (gx * gx + gy * gy)) * fmax(det, detp);
@@ -239,10 +243,10 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     const unsigned nbytes = (unsigned)(((Eb * NP + shift) * 8 + 15) & ~15);
     tma = (gbase + nbytes / 8 <= K * NP);
     if (tid == TMA_T) {
-      const unsigned rec = (unsigned)Eb * 32u + (unsigned)Eb * 96u;
+      const unsigned rec = (unsigned)Eb * 32u + (unsigned)Eb * (8u * GF);
       mbar_add_tx(mbar, rec + (tma ? nbytes * (1u + (with_p ? 1u : 0u)) : 0u));
       tma_load_1d(gG, a.gG + e0, (unsigned)Eb * 32u, mbar);
-      tma_load_1d(sb + L.o_gF, a.gF + e0 * GF, (unsigned)Eb * 96u, mbar);
+      tma_load_1d(sb + L.o_gF, a.gF + e0 * GF, (unsigned)Eb * (8u * GF), mbar);
       if (tma) {
         tma_load_1d(sb + L.o_u0, U + gbase, nbytes, mbar);
         if (with_p) tma_load_1d(sb + L.o_u1, pold + gbase, nbytes, mbar);
