@@ -416,6 +416,67 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------- NEXT rows, measured on C2
+def run_next(args):
+    """NEXT-1: screened Poisson -L + lambda with the block-Jacobi scaled inverse mass vs point
+    Jacobi -- iterations to 1e-8, device time per iteration, solves/s.  NEXT-2: DG gradient / divergence
+    (Eqs. INS_SD_4_1/4_2) -- time per call and GB/s on algorithmic bytes (read 1 or 2 fields, write 2 or 1,
+    + 48 B of geometry/connectivity per element)."""
+    import torch
+    from paper_1801_00246_b200 import Ipdg, meshgen
+    pk = peaks()
+    mesh = meshgen.square(C2["nx"], jitter=C2["jitter"], diag=C2["diag"], order=C2["order"], seed=C2["seed"])
+    stream = torch.cuda.current_stream()
+    for N in (4, 8):
+        op = Ipdg(N, mesh)
+        K, Np = op.K, op.Np
+        x_nodes, y_nodes = op.nodes()
+        f = math.pi ** 2 * 2 * torch.sin(math.pi * x_nodes) * torch.sin(math.pi * y_nodes)
+        rhs = {"smooth sin(pi x) sin(pi y)": op.mass(f),
+               "random U(-1,1)": op.mass(torch.from_numpy(meshgen.uniform_field(K, Np, seed=77)).cuda())}
+        for (rname, b), lam, pc in [(r, l, q) for r in rhs.items() for l in (1e5, 1e3) for q in (2, 1)]:
+            if True:
+                op.pcg_solve(b, torch.zeros_like(b), lam=lam, precond=pc, tol=1e-8, maxit=2)  # setup, graphs
+                x = torch.zeros_like(b)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                _, st = op.pcg_solve(b, x, lam=lam, precond=pc, tol=1e-8, maxit=20000)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                x = torch.zeros_like(b)
+                op.pcg_begin(b, x, lam=lam, precond=pc, tol=0.0)
+                op.pcg_iterate_profiled(3)
+                ma, mb = op.pcg_iterate_profiled(50)
+                op.pcg_end()
+                print(json.dumps({"next": "NEXT-1 screened Poisson PCG", "config": "C2 mesh", "N": N, "K": K, "lambda": lam, "rhs": rname,
+                                  "precond": {1: "jacobi", 2: "block-jacobi (scaled inverse mass)"}[pc],
+                                  "iterations": st["iterations"], "rel_residual": st["rel_residual"], "solve_ms": round(ms, 3),
+                                  "solves_per_s": round(1e3 / ms, 2), "pass_a_us": round(1e3 * ma / 50, 2),
+                                  "pass_b_us": round(1e3 * mb / 50, 2)}), flush=True)
+        p = torch.rand(K, Np, dtype=torch.float64, device="cuda")
+        uy = torch.rand_like(p)
+        for name, fn, nin, nout in (("G p", lambda: op.dg_grad(p), 1, 2), ("D u", lambda: op.dg_div(p, uy), 2, 1)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(50):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 50
+            byt = (8 * Np * (nin + nout) + 48) * K
+            print(json.dumps({"next": "NEXT-2 DG %s (central fluxes)" % name, "config": "C2 mesh", "N": N, "K": K,
+                              "us": round(1e3 * ms, 2), "gdofs": round(K * Np / (ms / 1e3) / 1e9, 2),
+                              "hbm_gbs_algorithmic": round(byt / (ms / 1e3) / 1e9, 1),
+                              "hbm_frac": round(byt / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)}), flush=True)
+        del op
+        torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- degree sweep (C3), Ax only
 def run_sweep(args):
     import torch
@@ -473,6 +534,7 @@ def main():
     ap.add_argument("--ref-nx", type=int, default=50)
     ap.add_argument("--variant", type=int, default=0, help="operator kernel variant (0 auto)")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--next", action="store_true", help="NEXT-1 / NEXT-2 measurements (SURVEY 8.6) on the C2 mesh")
     ap.add_argument("--sweep-nx", type=int, default=707)
     ap.add_argument("--sweep-variants", type=int, nargs="+", default=[0], help="0 auto, 1 fused, 2 split, 3 thread-per-element (N<=4)")
     args = ap.parse_args()
@@ -482,6 +544,8 @@ def main():
         run_reference(args)
     elif args.sweep:
         run_sweep(args)
+    elif args.next:
+        run_next(args)
     else:
         run_ours(args)
 
