@@ -107,6 +107,15 @@ struct ipdg_ctx_s {
   double gkey_lambda = -1.0;
   int gkey_precond = -1;
   cudaStream_t cap_stream = nullptr;
+  // split pass A (k_pipe): interior blocks, then halo-boundary blocks once the exchange (on comm_stream)
+  // has landed -- the halo exchange overlaps the interior work
+  bool split_a = false;        // multi-GPU halo, or forced for tests (ipdg_debug_split_pass_a)
+  int force_split = 0;
+  int* blist = nullptr;        // [interior block ids | boundary block ids]
+  int nb_split[2] = {0, 0};
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+  bool halo_ev_pending = false;
   // pending host mesh (ipdg_upload_mesh -> ipdg_upload_halo)
   int64_t pend_K = 0, pend_remote = 0;
   std::vector<int> pend_etoe, pend_etof;
@@ -633,11 +642,23 @@ struct Impl {
     if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
     if (k == 4) {
       const int gp = c->grid_pipe[1][lam];
-      if (lam) k_pipe<N, MODE_PCG_A, true><<<gp, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
-      else k_pipe<N, MODE_PCG_A, false><<<gp, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
+      auto launch = [&](int part, const int* list, int n) -> int {
+        a.blist = list;
+        a.nlist = n;
+        a.red_part = part;
+        const int g = list ? std::max(1, std::min(gp, n)) : gp;
+        if (lam) k_pipe<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
+        else k_pipe<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
+        c->launches++;
+        CUDA_TRY(c, cudaGetLastError());
+        return IPDG_OK;
+      };
+      if (c->split_a) {  // interior blocks, (wait for the halo exchange), halo-boundary blocks
+        TRY(launch(1, c->blist, c->nb_split[0]));
+        if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+        return launch(2, c->blist + c->nb_split[0], c->nb_split[1]);
+      }
+      return launch(0, nullptr, 0);
     }
     const int g = c->grid[1][lam];
     if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1][1], s>>>(a, c->gmax);
@@ -866,7 +887,10 @@ int ipdg_create(ipdg_ctx* out, int N, int device) {
   }
   if (cudaMalloc(&c->st, sizeof(PcgState)) != cudaSuccess || cudaMallocHost(&c->st_host, sizeof(PcgState)) != cudaSuccess ||
       cudaMalloc(&c->counter, sizeof(unsigned int)) != cudaSuccess || cudaMemset(c->counter, 0, sizeof(unsigned int)) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return IPDG_ECUDA;
   }
@@ -884,6 +908,10 @@ int ipdg_destroy(ipdg_ctx c) {
     if (p) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->blist) cudaFree(c->blist);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return IPDG_OK;
@@ -1019,6 +1047,29 @@ static Schedule build_schedule(int64_t K, int E, int gcap, const std::vector<int
   return S;
 }
 
+// interior / halo-boundary block lists of the split pass A (a block is boundary when one of its ghosts
+// is a halo ghost, id >= K); with force_split (tests) odd blocks count as boundary
+static int build_block_lists(ipdg_ctx c, int64_t K, const std::vector<int>& boff, const std::vector<int>& goff,
+                             const std::vector<int>& gid) {
+  const int nb = (int)boff.size() - 1;
+  std::vector<int> in, bd;
+  bool any_halo = false;
+  for (int b = 0; b < nb; ++b) {
+    bool halo = false;
+    for (int g = goff[b]; g < goff[b + 1]; ++g) halo |= gid[g] >= K;
+    any_halo |= halo;
+    if (c->force_split ? (b & 1) : halo) bd.push_back(b);
+    else in.push_back(b);
+  }
+  c->nb_split[0] = (int)in.size();
+  c->nb_split[1] = (int)bd.size();
+  in.insert(in.end(), bd.begin(), bd.end());
+  if (in.empty()) in.push_back(0);
+  TRY(upload(c, &c->blist, in.data(), in.size()));
+  c->split_a = any_halo || c->force_split != 0;
+  return IPDG_OK;
+}
+
 static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   const int64_t K = c->pend_K;
   const int E = c->E;
@@ -1053,6 +1104,7 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   TRY(upload(c, &c->goff, goff.data(), goff.size()));
   TRY(upload(c, &c->gid, gid.data(), gid.size()));
   TRY(upload(c, &c->boff, boff.data(), boff.size()));
+  TRY(build_block_lists(c, K, boff, goff, gid));
   TRY(upload(c, &c->etoe, etoe.data(), etoe.size()));
   TRY(upload(c, &c->bcode, bcv.data(), bcv.size()));
   c->etoe_h = etoe;
@@ -1358,9 +1410,34 @@ static int pass_b(ipdg_ctx c, cudaStream_t s) {
   return IPDG_OK;
 }
 
+static int resolved_pass_a(ipdg_ctx c) {
+  const bool lam = c->lambda != 0.0;
+  switch (c->N) {
+    case 1: return Impl<1>::resolve(c, 1, lam, c->x); case 2: return Impl<2>::resolve(c, 1, lam, c->x);
+    case 3: return Impl<3>::resolve(c, 1, lam, c->x); case 4: return Impl<4>::resolve(c, 1, lam, c->x);
+    case 5: return Impl<5>::resolve(c, 1, lam, c->x); case 6: return Impl<6>::resolve(c, 1, lam, c->x);
+    case 7: return Impl<7>::resolve(c, 1, lam, c->x); default: return Impl<8>::resolve(c, 1, lam, c->x);
+  }
+}
+
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
-  TRY(halo_for_p(c, s));
-  TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
+  if (c->split_a && resolved_pass_a(c) == 4) {
+    // halo exchange of p_k on the comm stream, overlapping the interior blocks of pass A
+    c->halo_ev_pending = false;
+    if ((c->H > 0 || c->S > 0) && !c->halo_external) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+      TRY(halo_for_p(c, c->comm_stream));
+      CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+      c->halo_ev_pending = true;
+    }
+    const int rc = [&]() -> int { DISPATCH(c->N, pass_a(c, s)); }();
+    c->halo_ev_pending = false;
+    TRY(rc);
+  } else {
+    TRY(halo_for_p(c, s));
+    TRY([&]() -> int { DISPATCH(c->N, pass_a(c, s)); }());
+  }
   TRY(allreduce(c, &c->st->red_A, 1, s));
   TRY(pass_b(c, s));
   TRY(allreduce(c, c->st->red_B, 2, s));
@@ -1690,6 +1767,24 @@ int ipdg_debug_phase_cycles(unsigned long long* out8, int reset) {
 #else
   for (int i = 0; i < 8; ++i) out8[i] = 0;
 #endif
+  return IPDG_OK;
+}
+
+// debug (not in ipdg.h): force the split pass A (interior / boundary block lists, odd blocks as
+// "boundary") on a single partition, to test the two-launch reduction without a halo.  Re-uploads the
+// block lists; call after ipdg_upload_mesh.
+int ipdg_debug_split_pass_a(ipdg_ctx c, int on) {
+  if (!c || c->K == 0) return IPDG_EINVAL;
+  c->force_split = on ? 1 : 0;
+  std::vector<int> boff(c->nblocks + 1), goff(c->nblocks + 1);
+  CUDA_TRY(c, cudaMemcpy(boff.data(), c->boff, boff.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(goff.data(), c->goff, goff.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int> gid(std::max(1, goff.back()));
+  if (goff.back() > 0) CUDA_TRY(c, cudaMemcpy(gid.data(), c->gid, goff.back() * sizeof(int), cudaMemcpyDeviceToHost));
+  TRY(build_block_lists(c, c->K, boff, goff, gid));
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->gkey_x = nullptr;
   return IPDG_OK;
 }
 

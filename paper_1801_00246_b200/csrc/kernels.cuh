@@ -72,6 +72,9 @@ struct AxArgs {
   int64_t K;             // local elements
   int64_t H;             // halo ghosts (rows of halo_p)
   int nblocks;           // element blocks (contiguous ranges of <= E own elements)
+  const int* blist;      // k_pipe: null = all blocks, else process blocks blist[0..nlist) (split pass A)
+  int nlist;
+  int red_part;          // k_pipe PCG: 0 = p.Ap -> red_A; 1 = -> red_A_part; 2 = red_A = red_A_part + own
   const int* boff;       // [nblocks+1] first element of each block
   const double4* geo;    // [K + H] r_x, s_x, r_y, s_y  (H = halo ghosts, multi-GPU)
   const short4* nbr;     // [K] per face: slot (x,y,z), w = flags: face f -> bits 4f..4f+3 = (f' | bc << 2)
@@ -104,6 +107,7 @@ struct AxArgs {
 struct PcgState {
   double rho_hist[4];  // rho_k = r_k . z_k at slot k & 3 (global values)
   double red_A;        // sigma_k = p_k . A p_k  (pass-A output, all-reduced in place)
+  double red_A_part;   // first half of a split pass A (interior blocks)
   double red_B[3];     // (rho_k, rr_k, bb) pass-B / init output, all-reduced in place
   double bb;           // ||b||^2
   double tol2;         // tol^2

@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t K = a.K;
   const int G = gridDim.x;
+  // blocks to process: all (list position = block id), or the ids in a.blist (interior / halo-boundary
+  // subsets of a split pass A, overlapping the halo exchange)
+  const int nbl = a.blist ? a.nlist : a.nblocks;
+  auto bid = [&](int j) -> int { return a.blist ? a.blist[j] : j; };
 
   PcgDecision d;
   double dot = 0.0;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
       const int j = tid >> 2, w = tid & 3;
       const int b = blockIdx.x + j * G;
       int v = 0;
-      if (b < a.nblocks) v = (w < 2) ? a.boff[b + w] : a.goff[b + w - 2];
+      if (b < nbl) v = (w < 2) ? a.boff[bid(b) + w] : a.goff[bid(b) + w - 2];
       meta[4 * j + w] = v;
     }
     for (int i = tid; i < 2 * L.sz; i += NTHR) sm[L.stg + i] = 0.0;  // padding rows stay finite
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (blockIdx.x < a.nblocks) {  // ghost ids of block 0 (plain loads, once)
+    if (blockIdx.x < nbl) {  // ghost ids of block 0 (plain loads, once)
       const int g0 = meta[2], g1 = meta[3];
       for (int g = tid; g < g1 - g0; g += NTHR) gids0[g] = a.gid[g0 + g];
     }
@@ -375,13 +379,13 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
 
   int cur_shift = 0, nxt_shift = 0;
   bool cur_tma = false, nxt_tma = false;
-  if (blockIdx.x < a.nblocks) {
+  if (blockIdx.x < nbl) {
     issue(sm + L.stg, meta, gids0, cur_shift, cur_tma);
     if (with_x) issue_x(meta);
     __syncthreads();  // every thread has registered its copies
     if (tid == TMA_T) mbar_arrive(mbar);
     const int b1 = blockIdx.x + G;
-    if (b1 < a.nblocks) {  // ghost ids of block 1 -> gids[1]
+    if (b1 < nbl) {  // ghost ids of block 1 -> gids[1]
       const int g0 = meta[4 + 2], g1 = meta[4 + 3];
       for (int g = tid; g < g1 - g0; g += NTHR) cp_async4(gids0 + gm8 + g, a.gid + g0 + g);
     }
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
 #endif
   double wr[NT][2], ws[NT][2];
   int it = 0;
-  for (int b = blockIdx.x; b < a.nblocks; b += G, ++it) {
+  for (int b = blockIdx.x; b < nbl; b += G, ++it) {
     const int par = it & 1;
     const int* mt = meta + 4 * (it & 3);
     const int64_t e0 = mt[0];
@@ -422,18 +426,19 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     // ---- issue block b + G into the other buffer, ghost ids of block b + 2G, metadata of b + 3G
     {
       const int b1 = b + G, b2 = b + 2 * G, b3 = b + 3 * G;
-      if (b1 < a.nblocks)
+      if (b1 < nbl)
         issue(sm + L.stg + (par ^ 1) * L.sz, meta + 4 * ((it + 1) & 3), gids0 + (par ^ 1) * gm8, nxt_shift, nxt_tma);
-      if (b2 < a.nblocks) {
+      if (b2 < nbl) {
         const int* m2 = meta + 4 * ((it + 2) & 3);
         const int g0 = m2[2], g1 = m2[3];
         int* gdst = gids0 + par * gm8;
         for (int g = tid; g < g1 - g0; g += NTHR) cp_async4(gdst + g, a.gid + g0 + g);
       }
-      if (tid < 4 && b3 < a.nblocks) {
+      if (tid < 4 && b3 < nbl) {
         int* m3 = meta + 4 * ((it + 3) & 3);
-        if (tid < 2) cp_async4(m3 + tid, a.boff + b3 + tid);
-        else cp_async4(m3 + tid, a.goff + b3 + tid - 2);
+        const int b3i = bid(b3);
+        if (tid < 2) cp_async4(m3 + tid, a.boff + b3i + tid);
+        else cp_async4(m3 + tid, a.goff + b3i + tid - 2);
       }
       cp_async_commit();
     }
@@ -544,8 +549,8 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     PHASE_MARK(3);  // P1 + volume DMMAs (warp 0)
     __syncthreads();  // traces of every slot written; x rows of this block consumed
     PHASE_MARK(4);  // barrier
-    if (tid == TMA_T && b + G < a.nblocks) mbar_arrive(mbar);  // block b + G: every copy is registered
-    if (with_x && b + G < a.nblocks) issue_x(meta + 4 * ((it + 1) & 3));
+    if (tid == TMA_T && b + G < nbl) mbar_arrive(mbar);  // block b + G: every copy is registered
+    if (with_x && b + G < nbl) issue_x(meta + 4 * ((it + 1) & 3));
 
     // ---- P2 + P3 face part per warp on its own tile
     if (8 * warp < Eb) {
@@ -624,7 +629,10 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     double v[1] = {dot}, out[1];
     if (grid_reduce<1>(v, red, a.partials, a.counter, out)) {
       PcgState* st = a.st;
-      st->red_A = out[0];
+      // split pass A: the first launch parks its partial p.Ap, the second adds it (red_A is still read
+      // as alpha_{k-1}'s denominator by the second launch's prologue)
+      if (a.red_part == 1) st->red_A_part = out[0];
+      else st->red_A = (a.red_part == 2) ? st->red_A_part + out[0] : out[0];
       st->rho_hist[(d.k - 1) & 3] = d.rhoB;
       if (d.first) st->bb = d.bbv;
     }

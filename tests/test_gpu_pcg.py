@@ -139,3 +139,27 @@ def test_block_jacobi_needs_positive_lambda():
     b = torch.ones(op.K, op.Np, dtype=torch.float64, device="cuda")
     with pytest.raises(IpdgError):
         op.pcg_solve(b, precond=2, lam=0.0)
+
+
+@pytest.mark.parametrize("N", [3, 4, 5])
+def test_split_pass_a_two_launch_reduction(N):
+    """The multi-GPU pass A runs interior blocks, then halo-boundary blocks after the exchange, with p.Ap
+    summed over the two launches (AxArgs::red_part).  Forced on one partition (odd blocks as the second
+    launch) it must give the oracle's PCG (iterations within R15, residual)."""
+    import ctypes
+    from paper_1801_00246_b200 import _lib
+    m = meshgen.square(12, jitter=0.2, diag="random", order="morton", seed=17)
+    ref = RefElem(N)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, meshgen.sin_sin_forcing)
+    op = Ipdg(N, m)
+    op.set_variant(4)
+    fn = _lib.lib().ipdg_debug_split_pass_a
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    assert fn(op.ctx, 1) == 0
+    x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-9, maxit=5000)
+    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-9, 5000, dinv=1.0 / A.diagonal())
+    assert st["status"] == sto["status"] == 0
+    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    r = b.ravel() - A @ x.cpu().numpy().ravel()
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b) * 1.01
