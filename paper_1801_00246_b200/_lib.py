@@ -77,6 +77,7 @@ def lib():
     if _LIB is None:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError("libipdg.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
+        import torch  # noqa: F401  -- torch's CUDA/NCCL libraries first; libipdg links the same libnccl.so.2
         L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)

@@ -16,7 +16,7 @@ flags = [f for f in sys.argv[2:] if f.startswith("-D")]
 out = os.path.join(ROOT, "exp_so", "libipdg_exp_%s.so" % "_".join(f[2:] for f in flags) if flags else "base")
 if not os.path.exists(out):
     fl = [f for f in B.FLAGS if f not in ("-Xptxas", "-v")]
-    cmd = [B.NVCC] + fl + flags + [os.path.join(B.CSRC, x) for x in B.SOURCES] + ["-o", out, "-lnccl"]
+    cmd = [B.NVCC] + fl + B.nccl_flags()[0] + flags + [os.path.join(B.CSRC, x) for x in B.SOURCES] + ["-o", out] + B.nccl_flags()[1]
     subprocess.run(cmd, check=True, capture_output=True)
 import paper_1801_00246_b200._lib as L  # noqa: E402
 L.LIB_PATH = out

@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 from paper_1801_00246_b200 import build as B  # noqa: E402
 
 out = "/tmp/libipdg_timing.so"
-cmd = [B.NVCC] + B.FLAGS + ["-DIPDG_PHASE_TIMING"] + [os.path.join(B.CSRC, x) for x in B.SOURCES] + ["-o", out, "-lnccl"]
+cmd = [B.NVCC] + B.FLAGS + B.nccl_flags()[0] + ["-DIPDG_PHASE_TIMING"] + [os.path.join(B.CSRC, x) for x in B.SOURCES] + ["-o", out] + B.nccl_flags()[1]
 subprocess.run(cmd, check=True, capture_output=True)
 import paper_1801_00246_b200._lib as L  # noqa: E402
 L.LIB_PATH = out
