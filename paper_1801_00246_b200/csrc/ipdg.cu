@@ -135,6 +135,7 @@ struct ipdg_ctx_s {
   int nranks = 1, rank = 0;
   std::string err;
   int64_t launches = 0;
+  int launches_per_iter = 2;  // kernels per PCG iteration (set when the iteration graph is captured)
 };
 
 static constexpr int kChunk = 32;
@@ -528,7 +529,25 @@ struct Impl {
     a.tau_c = c->tau_c;
     a.halo = c->halobuf;
     a.W2 = c->W2;
+    a.ebeg = 0;
+    a.eend = c->K + c->H;
+    a.stop_work = 1;
     return a;
+  }
+
+  // k_grad over [K, K + H) alone: the halo rows, once the exchange has landed
+  static int grad_launch(ipdg_ctx c, SplitArgs a, int mode, int64_t ebeg, int64_t eend, int stop_work, cudaStream_t s) {
+    using S = TrS<N>;
+    a.ebeg = ebeg;
+    a.eend = eend;
+    a.stop_work = stop_work;
+    const int64_t tiles = std::max<int64_t>(1, (eend - ebeg + 7) / 8);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)c->grid_grad));
+    if (mode == 0) k_grad<N, MODE_AX><<<g, S::W * 32, c->smem_grad, s>>>(a);
+    else k_grad<N, MODE_PCG_A><<<g, S::W * 32, c->smem_grad, s>>>(a);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
   }
 
   static int ensure_w2(ipdg_ctx c) {
@@ -545,10 +564,16 @@ struct Impl {
     a.Au = Au;
     a.lambda = lambda;
     using S = TrS<N>;
-    k_grad<N, MODE_AX><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+    if (c->H > 0) {  // own rows, then halo rows (the same split as the overlapped PCG pass A)
+      TRY(grad_launch(c, a, 0, 0, c->K, 1, s));
+      TRY(grad_launch(c, a, 0, c->K, c->K + c->H, 0, s));
+    } else {
+      k_grad<N, MODE_AX><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+      c->launches++;
+    }
     if (lambda != 0.0) k_flux<N, MODE_AX, true><<<c->grid_flux[0][1], S::W * 32, c->smem_flux[1], s>>>(a);
     else k_flux<N, MODE_AX, false><<<c->grid_flux[0][0], S::W * 32, c->smem_flux[0], s>>>(a);
-    c->launches += 2;
+    c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return IPDG_OK;
   }
@@ -567,10 +592,17 @@ struct Impl {
     a.partials = c->partials;
     a.counter = c->counter;
     using S = TrS<N>;
-    k_grad<N, MODE_PCG_A><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+    if (c->H > 0) {  // own rows overlap the halo exchange (comm stream); halo rows once it has landed
+      TRY(grad_launch(c, a, 1, 0, c->K, 1, s));
+      if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+      TRY(grad_launch(c, a, 1, c->K, c->K + c->H, 0, s));
+    } else {
+      k_grad<N, MODE_PCG_A><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
+      c->launches++;
+    }
     if (c->lambda != 0.0) k_flux<N, MODE_PCG_A, true><<<c->grid_flux[1][1], S::W * 32, c->smem_flux[1], s>>>(a);
     else k_flux<N, MODE_PCG_A, false><<<c->grid_flux[1][0], S::W * 32, c->smem_flux[0], s>>>(a);
-    c->launches += 2;
+    c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return IPDG_OK;
   }
@@ -1421,7 +1453,8 @@ static int resolved_pass_a(ipdg_ctx c) {
 }
 
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
-  if (c->split_a && resolved_pass_a(c) == 4) {
+  const int kern = resolved_pass_a(c);
+  if (c->split_a && (kern == 4 || (kern == 2 && c->H > 0))) {
     // halo exchange of p_k on the comm stream, overlapping the interior blocks of pass A
     c->halo_ev_pending = false;
     if ((c->H > 0 || c->S > 0) && !c->halo_external) {
@@ -1448,7 +1481,10 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
   cudaGraph_t g = nullptr;
   CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
   int rc = IPDG_OK;
+  const int64_t l0 = c->launches;
   for (int i = 0; i < iters && rc == IPDG_OK; ++i) rc = one_iteration(c, c->cap_stream);
+  c->launches_per_iter = (int)((c->launches - l0) / std::max(1, iters));  // kernels in one replayed iteration
+  c->launches = l0;  // captured, not launched
   cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
   if (rc != IPDG_OK) {
     if (g) cudaGraphDestroy(g);
@@ -1537,12 +1573,12 @@ int ipdg_pcg_iterate(ipdg_ctx c, int64_t n, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   while (n >= kChunk) {
     CUDA_TRY(c, cudaGraphLaunch(c->gexec[1], s));
-    c->launches += 2 * kChunk;
+    c->launches += (int64_t)c->launches_per_iter * kChunk;
     n -= kChunk;
   }
   while (n-- > 0) {
     CUDA_TRY(c, cudaGraphLaunch(c->gexec[0], s));
-    c->launches += 2;
+    c->launches += c->launches_per_iter;
   }
   return IPDG_OK;
 }

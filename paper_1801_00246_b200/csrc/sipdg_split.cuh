@@ -19,6 +19,8 @@ namespace ipdg {
 
 struct SplitArgs {
   int64_t K, H;
+  int64_t ebeg, eend;    // k_grad: element rows [ebeg, eend) of the K + H (own | halo) rows
+  int stop_work;         // k_grad PCG: this launch applies the deferred x update when the loop stops
   const double4* geo;    // [K+H]
   const int4* nbg;       // [K] neighbour element per face (>= K: halo ghost) + flags (f' | bc << 2) << 4f in .w
   const double* tables;  // G | M | L | aux | M2 (natural w rows)
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
     pnew = (d.k & 1) ? a.p_odd : a.p_even;
     pold = (d.k & 1) ? a.p_even : a.p_odd;
     if (d.stop) {  // deferred x update only; k_flux records the decision
+      if (!a.stop_work) return;
       const int64_t n = K * NP;
       for (int64_t i = blockIdx.x * (int64_t)blockDim.x + tid; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (d.zero_x) a.x[i] = 0.0;
@@ -107,10 +110,12 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
   double* st8 = stage + warp * 8 * SU;
   for (int i = lane; i < 8 * SU; i += 32) st8[i] = 0.0;
   __syncthreads();
-  const int64_t ntiles = (KH + 7) / 8;
+  // rows [ebeg, eend): all K + H rows, or the own rows and then the halo rows (the latter after the
+  // halo exchange, which the own rows overlap)
+  const int64_t ntiles = (a.eend - a.ebeg + 7) / 8;
   for (int64_t t = (int64_t)blockIdx.x * W + warp; t < ntiles; t += (int64_t)gridDim.x * W) {
-    const int64_t e0 = 8 * t;
-    const int nrow = (int)min((int64_t)8, KH - e0);
+    const int64_t e0 = a.ebeg + 8 * t;
+    const int nrow = (int)min((int64_t)8, a.eend - e0);
     __syncwarp();
     for (int q = lane; q < nrow * NP; q += 32) {  // operand rows of the tile (contiguous for own rows)
       const int el = q / NP, i = q - el * NP;
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
       for (int q = 0; q < 2 * NT; ++q) dmma(acc[q][0], acc[q][1], av, bt[q * 32]);
     }
     const int64_t e = e0 + (lane >> 2);
-    if (e < KH) {
+    if (e < a.eend) {
       const double4 g = a.geo[e];
       const double rx = g.x, sx = g.y, ry = g.z, sy = g.w;
       const double J = 1.0 / (rx * sy - sx * ry);
