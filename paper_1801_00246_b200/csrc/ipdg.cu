@@ -139,6 +139,7 @@ struct ipdg_ctx_s {
 };
 
 static constexpr int kChunk = 32;
+static constexpr int kCommSlots = 8;  // CTA slots left free for NCCL during an overlapped pass
 
 #define FAIL(ctx, code, ...)                                         \
   do {                                                              \
@@ -536,13 +537,14 @@ struct Impl {
   }
 
   // k_grad over [K, K + H) alone: the halo rows, once the exchange has landed
-  static int grad_launch(ipdg_ctx c, SplitArgs a, int mode, int64_t ebeg, int64_t eend, int stop_work, cudaStream_t s) {
+  static int grad_launch(ipdg_ctx c, SplitArgs a, int mode, int64_t ebeg, int64_t eend, int stop_work, cudaStream_t s,
+                         int spare = 0) {
     using S = TrS<N>;
     a.ebeg = ebeg;
     a.eend = eend;
     a.stop_work = stop_work;
     const int64_t tiles = std::max<int64_t>(1, (eend - ebeg + 7) / 8);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)c->grid_grad));
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)c->grid_grad - spare));
     if (mode == 0) k_grad<N, MODE_AX><<<g, S::W * 32, c->smem_grad, s>>>(a);
     else k_grad<N, MODE_PCG_A><<<g, S::W * 32, c->smem_grad, s>>>(a);
     c->launches++;
@@ -593,7 +595,7 @@ struct Impl {
     a.counter = c->counter;
     using S = TrS<N>;
     if (c->H > 0) {  // own rows overlap the halo exchange (comm stream); halo rows once it has landed
-      TRY(grad_launch(c, a, 1, 0, c->K, 1, s));
+      TRY(grad_launch(c, a, 1, 0, c->K, 1, s, c->halo_ev_pending ? kCommSlots : 0));
       if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
       TRY(grad_launch(c, a, 1, c->K, c->K + c->H, 0, s));
     } else {
@@ -678,7 +680,10 @@ struct Impl {
         a.blist = list;
         a.nlist = n;
         a.red_part = part;
-        const int g = list ? std::max(1, std::min(gp, n)) : gp;
+        // while the exchange is in flight leave a few CTA slots free for NCCL's kernel (the persistent grid
+        // would otherwise fill every SM and the exchange could only start after the interior blocks)
+        const int cap = (part == 1 && c->halo_ev_pending) ? std::max(1, gp - kCommSlots) : gp;
+        const int g = list ? std::max(1, std::min(cap, n)) : gp;
         if (lam) k_pipe<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
         else k_pipe<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
         c->launches++;
