@@ -372,9 +372,6 @@ struct Impl {
           CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
           int occ = 0;
           CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
-#ifdef IPDG_EXP_PIPE_ONE_CTA
-          occ = std::min(occ, 1);
-#endif
           if (occ > best) {
             best = occ;
             c->smem_pipe[mode][lam] = bytes;

@@ -266,46 +266,6 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
     double* gz = sb + L.o_g0;
     double* gp = sb + L.o_g1;
     int8_t* gs = reinterpret_cast<int8_t*>(sb + L.o_gs);
-#ifdef IPDG_GHOST_TMA
-    // ghosts (experiment, measured 1.8x slower than cp.async on C2: the bulk-copy unit serialises ~120
-    // small copies per block): one thread (the bulk-copy warp) issues a bulk copy per ghost record and per row span (the
-    // 16-byte-aligned span around the row); the others go straight to P1.  tx bytes are registered
-    // after the copies (the count may go transiently negative; the phase cannot complete before the
-    // arrival after the block barrier).
-    if (tid == TMA_T) {
-      unsigned tx = 0;
-      for (int g = 0; g < Gb; ++g) {
-        const int ge = gl[g];
-        const bool halo = ge >= K;
-        const double* base = halo ? a.halo_p : U;
-        const int64_t off = (halo ? (int64_t)(ge - K) : (int64_t)ge) * NP;
-        const int sh = (int)(off & 1);
-        const bool span = (off - sh + GSTR) <= (halo ? a.H : K) * NP;  // the span stays inside the array
-        double* dz = gz + g * GSTR;
-        double* dp = gp + g * GSTR;
-        tma_load_1d(gG + (E + g) * 4, a.gG + ge, 32u, mbar);
-        tx += 32u;
-        if (span) {
-          tma_load_1d(dz, base + off - sh, GSTR * 8u, mbar);
-          tx += GSTR * 8u;
-          if (with_p && !halo) {
-            tma_load_1d(dp, pold + off - sh, GSTR * 8u, mbar);
-            tx += GSTR * 8u;
-          }
-          gs[g] = (int8_t)sh;
-        } else {  // last row of the array: element-wise
-          for (int i = 0; i < NP; ++i) {
-            cp_async8(dz + i, base + off + i);
-            if (with_p && !halo) cp_async8(dp + i, pold + off + i);
-          }
-          gs[g] = 0;
-        }
-        if (with_p && halo)  // halo rows are already p_k (Ax: u); p_{k-1} row = 0
-          for (int i = 0; i < GSTR; ++i) dp[i] = 0.0;
-      }
-      mbar_add_tx(mbar, tx);
-    }
-#else
     // ghosts: records (2 x 16 B) and the 16-byte-aligned span around each row in 16-byte chunks
     for (int q = tid; q < 2 * Gb; q += NTHR) {
       const int g = q >> 1, h = q & 1;
@@ -339,7 +299,6 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
         }
       }
     }
-#endif
   };
 
   // ---- x rows of a block for the deferred update (issued once every warp has read the previous ones)
@@ -452,10 +411,8 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
         const double v = with_p ? fma(beta, po, wu[q]) : wu[q];
         const int64_t g = e0 * NP + q;
         wu[q] = v;
-#ifndef IPDG_EXP_NO_PSTORE
         pnew[g] = v;
         if (with_x) a.x[g] = fma(alpha_prev, po, xs[q]);
-#endif
       }
       if (with_p) {
         double* wg = sb + L.o_g0;
@@ -612,9 +569,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
           for (int h = 0; h < 2; ++h) {
             const int i = 8 * nt + 2 * (lane & 3) + h;
             if (i < NP) {
-#ifndef IPDG_EXP_NO_AUSTORE
               a.Au[base + i] = C[nt][h];
-#endif
               if (PCG) dot += uval(e, i) * C[nt][h];
             }
           }

@@ -1,7 +1,7 @@
-"""Timing experiments: build a copy of libipdg with extra -D flags (e.g. -DIPDG_EXP_NO_PSTORE) into /tmp and
+"""Timing experiments: build a copy of libipdg with extra -D flags into /tmp and
 report the C2 (N = 4) Ax and PCG pass A / pass B device times of the chosen variant.  Numbers only -- an
 experiment flag may make the results wrong on purpose.
-usage: python tools/exp_timing.py VARIANT [-DFLAG ...]"""
+usage: python tools/exp_timing.py VARIANT [-DFLAG ...]  (flags: any compile-time switch under test)"""
 import os
 import subprocess
 import sys
