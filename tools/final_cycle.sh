@@ -10,3 +10,6 @@ timeout 900 python bench.py --config C5 --steps 200 --no-cpu --no-solve > gpurun
 timeout 600 python bench.py --sweep > gpurun_out/${TAG}_sweep.jsonl 2>&1; cut -c1-100 gpurun_out/${TAG}_sweep.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-solve --no-e2e > gpurun_out/${TAG}_launches.log 2>&1; tail -1 gpurun_out/${TAG}_launches.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pipe -s 2 -c 2 -o gpurun_out/${TAG}_prof python tools/prof_run.py --N 4 --ax 2 --pcg 3 > gpurun_out/${TAG}_prof.log 2>&1; tail -1 gpurun_out/${TAG}_prof.log
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest.log 2>&1; tail -1 gpurun_out/${TAG}_pytest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; tail -1 gpurun_out/${TAG}_smoke.log
+timeout 900 python bench.py --next > gpurun_out/${TAG}_next.jsonl 2>&1; wc -l gpurun_out/${TAG}_next.jsonl
