@@ -110,3 +110,88 @@ constexpr int dgop_smem_doubles() {
 }
 
 }  // namespace ipdg
+
+#include "sipdg_tpe.cuh"
+
+namespace ipdg {
+
+// Low-degree variant (N <= 4): one thread per element, operators as compile-time indices into
+// __constant__ memory (c_tpe), the neighbour face values read from L1/L2 (as k_gather) -- no shared
+// memory, no block barriers.  Same formulas as k_dgop.
+template <int N, bool DIV>
+__global__ void __launch_bounds__(256) k_dgop_tpe(int64_t K, const double* __restrict__ f0, const double* __restrict__ f1,
+                                                  const double4* __restrict__ geo, const int4* __restrict__ nbg,
+                                                  double* __restrict__ o0, double* __restrict__ o1) {
+  using T = TrT<N>;
+  constexpr int NP = T::NP, NFP = T::NFP, NF3 = T::NF3;
+  const double* C = c_tpe<N>;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  double u0[NP], u1[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    u0[i] = f0[e * NP + i];
+    u1[i] = DIV ? f1[e * NP + i] : 0.0;
+  }
+  const double4 g = geo[e];
+  const int4 nb = nbg[e];
+  double j0[NF3], j1[NF3];  // G: g_x [[p]], g_y [[p]];  DIV: g.[[u]] in j0
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    const int fl = (nb.w >> (4 * f)) & 15;
+    const int fp = fl & 3, bc = fl >> 2;
+    const double gx = (f == 0) ? -g.y : (f == 1) ? g.x + g.y : -g.x;
+    const double gy = (f == 0) ? -g.w : (f == 1) ? g.z + g.w : -g.z;
+    const bool inner = (bc == 0);
+    const int64_t n = (f == 0) ? nb.x : (f == 1) ? nb.y : nb.z;
+    const bool flip = (f == 2) == (fp == 2);
+    const double sgn = DIV ? (bc == 1 ? 1.0 : -1.0) : (bc == 1 ? -1.0 : 1.0);
+#pragma unroll
+    for (int k = 0; k < NFP; ++k) {
+      const int im = fmask_cf<N>(f, k);
+      double p0, p1 = 0.0;
+      if (inner) {
+        const int kp = flip ? NFP - 1 - k : k;
+        const int ip = (fp == 0) ? fmask_cf<N>(0, kp) : (fp == 1) ? fmask_cf<N>(1, kp) : fmask_cf<N>(2, kp);
+        p0 = f0[n * NP + ip];
+        if (DIV) p1 = f1[n * NP + ip];
+      } else {
+        p0 = sgn * u0[im];
+        if (DIV) p1 = sgn * u1[im];
+      }
+      const double d0 = p0 - u0[im];  // [[w]] = w+ - w-
+      if (DIV) {
+        j0[f * NFP + k] = gx * d0 + gy * (p1 - u1[im]);
+      } else {
+        j0[f * NFP + k] = gx * d0;
+        j1[f * NFP + k] = gy * d0;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    double dr0 = 0.0, ds0 = 0.0, dr1 = 0.0, ds1 = 0.0, l0 = 0.0, l1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      dr0 = fma(C[T::O_DR + i * NP + j], u0[j], dr0);
+      ds0 = fma(C[T::O_DS + i * NP + j], u0[j], ds0);
+      if (DIV) {
+        dr1 = fma(C[T::O_DR + i * NP + j], u1[j], dr1);
+        ds1 = fma(C[T::O_DS + i * NP + j], u1[j], ds1);
+      }
+    }
+#pragma unroll
+    for (int fk = 0; fk < NF3; ++fk) {
+      l0 = fma(C[T::O_LIFT + i * NF3 + fk], j0[fk], l0);
+      if (!DIV) l1 = fma(C[T::O_LIFT + i * NF3 + fk], j1[fk], l1);
+    }
+    if (DIV) {
+      o0[e * NP + i] = g.x * dr0 + g.y * ds0 + g.z * dr1 + g.w * ds1 + 0.5 * l0;
+    } else {
+      o0[e * NP + i] = g.x * dr0 + g.y * ds0 + 0.5 * l0;
+      o1[e * NP + i] = g.z * dr0 + g.w * ds0 + 0.5 * l1;
+    }
+  }
+}
+
+}  // namespace ipdg

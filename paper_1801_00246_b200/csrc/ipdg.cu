@@ -427,6 +427,7 @@ struct Impl {
           h[TT::O_LSS + m * NP + n] = b;
         }
       for (int i = 0; i < NFP * NFP; ++i) h[TT::O_M1D + i] = R.M1D[i];
+      for (int i = 0; i < NP * NF3; ++i) h[TT::O_LIFT + i] = R.LIFT[i];
       CUDA_TRY(c, cudaMemcpyToSymbol(c_tpe<N>, h.data(), h.size() * sizeof(double)));
     }
     return IPDG_OK;
@@ -719,6 +720,14 @@ struct Impl {
 
   // DG gradient (div = false: o0, o1 = G p) or divergence (div = true: o0 = D u) with central fluxes
   static int dgop(ipdg_ctx c, bool div, const double* f0, const double* f1, double* o0, double* o1, cudaStream_t s) {
+    if constexpr (N <= 4) {  // thread per element, operators in constant memory
+      const int grid = (int)std::max<int64_t>(1, (c->K + 255) / 256);
+      if (div) k_dgop_tpe<N, true><<<grid, 256, 0, s>>>(c->K, f0, f1, c->geo, c->nbg, o0, nullptr);
+      else k_dgop_tpe<N, false><<<grid, 256, 0, s>>>(c->K, f0, nullptr, c->geo, c->nbg, o0, o1);
+      c->launches++;
+      CUDA_TRY(c, cudaGetLastError());
+      return IPDG_OK;
+    }
     constexpr int EPB = 256 / T::NP;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->K + EPB - 1) / EPB, (int64_t)c->sms * 8));
     if (div) {

@@ -34,7 +34,8 @@ struct TrT {
   static constexpr int O_LSS = O_LSR + NF3 * NP;
   static constexpr int O_M1D = O_LSS + NF3 * NP;       // [k][m]
   static constexpr int O_M = O_M1D + NFP * NFP;         // [n][j] reference mass (lambda term)
-  static constexpr int TOTAL = O_M + NP * NP;
+  static constexpr int O_LIFT = O_M + NP * NP;          // [n][fk] LIFT (DG gradient / divergence, dgops.cuh)
+  static constexpr int TOTAL = O_LIFT + NP * NF3;
 };
 
 template <int N>
