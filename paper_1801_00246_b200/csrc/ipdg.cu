@@ -528,6 +528,8 @@ struct Impl {
     a.tau_c = c->tau_c;
     a.halo = c->halobuf;
     a.W2 = c->W2;
+    a.gG = c->gG;
+    a.gF = c->gF;
     a.ebeg = 0;
     a.eend = c->K + c->H;
     a.stop_work = 1;

@@ -67,6 +67,10 @@ __host__ __device__ __forceinline__ constexpr int fmask_cf(int f, int k) {
   return f == 0 ? k : (f == 1 ? k * (N + 1) - (k * (k - 1)) / 2 + N - k : k * (N + 1) - (k * (k - 1)) / 2);
 }
 
+// per-element face record length (k_geofacs) in doubles: 9 used, padded to 10 so a block's records
+// (80 B each) are a 16-byte multiple for a bulk copy
+constexpr int kGF = 10;
+
 // Kernel parameters (plain pointers; all device memory).
 struct AxArgs {
   int64_t K;             // local elements

@@ -21,10 +21,6 @@
 
 namespace ipdg {
 
-// per-element face record length in doubles: 9 used, padded to 10 so a block's records (80 B each)
-// are a 16-byte multiple for the bulk copy
-constexpr int kGF = 10;
-
 template <int N>
 struct TrPipe {
   using T = Tr<N>;

@@ -19,6 +19,8 @@ namespace ipdg {
 
 struct SplitArgs {
   int64_t K, H;
+  const double4* gG;     // [K + H] (J G_rr, J G_rs, J G_ss, J) (k_geofacs)
+  const double* gF;      // [K][kGF] per face (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau)
   int64_t ebeg, eend;    // k_grad: element rows [ebeg, eend) of the K + H (own | halo) rows
   int stop_work;         // k_grad PCG: this launch applies the deferred x update when the loop stops
   const double4* geo;    // [K+H]
@@ -148,10 +150,8 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
     }
     const int64_t e = e0 + (lane >> 2);
     if (e < a.eend) {
-      const double4 g = a.geo[e];
-      const double rx = g.x, sx = g.y, ry = g.z, sy = g.w;
-      const double J = 1.0 / (rx * sy - sx * ry);
-      const double Grr = J * (rx * rx + ry * ry), Grs = J * (rx * sx + ry * sy), Gss = J * (sx * sx + sy * sy);
+      const double4 gr = a.gG[e];  // J G^T G from the setup records (k_geofacs)
+      const double Grr = gr.x, Grs = gr.y, Gss = gr.z;
       double* wrow = a.W2 + e * 2 * NP;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -228,26 +228,17 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_flux(SplitArgs a) {
     const bool valid = eraw < K;
     const int64_t e = valid ? eraw : e0;
     const int4 nb = a.nbg[e];
-    const double4 g = a.geo[e];
-    const double rx = g.x, sx = g.y, ry = g.z, sy = g.w;
-    const double det = rx * sy - sx * ry;
-    const double J = 1.0 / det;
-    // per-face coefficients: lane (element, f < 3) computes face f, the others read it by shuffle
+    // per-face coefficients (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau) from the setup records (k_geofacs):
+    // lane (element, f < 3) loads face f, the others read it by shuffle
     double ccr = 0.0, ccs = 0.0, cst = 0.0;
     {
       const int f = lane & 3;
-      const double gx = (f == 0) ? -sx : (f == 1) ? rx + sx : -rx;
-      const double gy = (f == 0) ? -sy : (f == 1) ? ry + sy : -ry;
-      const double sJ = J * sqrt(gx * gx + gy * gy);
-      const int bc = f < 3 ? (nb.w >> (4 * f + 2)) & 3 : 1;
-      double detp = 0.0;
-      if (bc == 0) {
-        const double4 h = a.geo[(f == 0) ? nb.x : (f == 1) ? nb.y : nb.z];
-        detp = h.x * h.w - h.y * h.z;
+      if (f < 3) {
+        const double* r = a.gF + e * kGF + 3 * f;
+        ccr = r[0];
+        ccs = r[1];
+        cst = r[2];
       }
-      ccr = 0.5 * J * (rx * gx + ry * gy);
-      ccs = 0.5 * J * (sx * gx + sy * gy);
-      cst = sJ * a.tau_c * sJ * fmax(det, detp);
     }
     const double* uo = U + e * NP;
     const double* wo = a.W2 + e * 2 * NP;
@@ -312,7 +303,7 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_flux(SplitArgs a) {
       }
     }
     if (LAM) {
-      const double lj = a.lambda * J;
+      const double lj = a.lambda * a.gG[e].w;  // lambda J
 #pragma unroll
       for (int kc = 0; kc < KCM; ++kc) {
         const int k = 4 * kc + (lane & 3);
