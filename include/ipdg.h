@@ -185,8 +185,8 @@ int ipdg_get_connectivity(ipdg_ctx ctx, int32_t* etoe, int32_t* etof, int64_t ca
  * k_sipdg, then the pass-A kernel the context resolves to for lambda = 0 (1 k_sipdg, 2 k_grad + k_flux,
  * 3 k_tpe, 4 k_pipe, 5 k_gather) with its smem bytes/CTA and grid */
 int ipdg_info(ipdg_ctx ctx, int64_t* out, int n);
-/* Operator kernel variant: 0 auto (the variant measured fastest for the degree: 5 for N <= 2, 4 for
- * N = 3..5, 2 for N >= 6), 1 fused single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels
+/* Operator kernel variant: 0 auto (the variant measured fastest for the degree and pass: Ax 5 for N <= 3,
+ * 4 for N = 4, 5, 2 for N >= 6; PCG pass A 5 for N = 1, 4 for N = 2..5, 2 for N >= 6), 1 fused single-kernel (k_sipdg, DMMA), 2 split gradient + flux kernels
  * (k_grad, k_flux, DMMA), 3 thread-per-element with block staging (k_tpe, DFMA with operators in
  * constant memory), 4 software-pipelined fused (k_pipe, DMMA, TMA-staged rows; falls back to 1 when an
  * operand is not 16-byte aligned or the block does not fit in shared memory), 5 gather (k_gather, one

@@ -489,13 +489,14 @@ struct Impl {
   // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
   // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe, 5 gather).
-  // Auto (variant 0): gather for N <= 2, pipelined fused for N = 3..5, split for N >= 6 --
-  // the fastest per degree on C3 Ax and on the C2 (N = 4) / C4 (N = 6) PCG steps
-  // (profiles/r01_sweep_pipe.jsonl, profiles/r01_bench_*.json).
+  // Auto (variant 0), the fastest measured per degree and pass: Ax -- gather for N <= 3, pipelined fused
+  // for N = 4, 5, split for N >= 6 (C3 sweep, profiles/r01_sweep_*.jsonl); PCG pass A -- gather for N = 1,
+  // pipelined fused for N = 2..5 (its p formation and x update are cheaper in the staged kernel:
+  // tools/pcg_lowN_timing.py on C2, N = 2: 47 vs 50 us, N = 3: 68 vs 74 us), split for N >= 6.
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N <= 2) ? 5 : (N <= 5 ? 4 : 2);
+    if (k == 0) k = (N >= 6) ? 2 : (N <= (mode == 0 ? 3 : 1) ? 5 : 4);
     if ((k == 3 || k == 5) && N > 4) k = 1;
     if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
     return k;
@@ -505,10 +506,10 @@ struct Impl {
   template <int MODE>
   static int launch_gather(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s) {
     if constexpr (N <= 4) {
-      const int grid = (int)std::max<int64_t>(1, (c->K + 255) / 256);  // one element per thread
+      const int grid = (int)std::max<int64_t>(1, (c->K + kGatherThreads - 1) / kGatherThreads);  // one element per thread
       if (MODE == MODE_PCG_A && grid > c->partials_cap) FAIL(c, IPDG_ECUDA, "partials buffer too small");
-      if (lam) k_gather<N, MODE, true><<<grid, 256, 0, s>>>(a);
-      else k_gather<N, MODE, false><<<grid, 256, 0, s>>>(a);
+      if (lam) k_gather<N, MODE, true><<<grid, kGatherThreads, 0, s>>>(a);
+      else k_gather<N, MODE, false><<<grid, kGatherThreads, 0, s>>>(a);
       c->launches++;
       CUDA_TRY(c, cudaGetLastError());
       return IPDG_OK;
@@ -1413,8 +1414,8 @@ static int ensure_ws(ipdg_ctx c) {
 }
 
 static int ensure_partials(ipdg_ctx c) {
-  // one slot per CTA of the largest reducing grid (k_gather: one CTA per 256 elements)
-  const int need = (int)std::max<int64_t>(std::max(4096, 4 * c->sms * 16), (c->K + 255) / 256);
+  // one slot per CTA of the largest reducing grid (k_gather: one CTA per kGatherThreads elements)
+  const int need = (int)std::max<int64_t>(std::max(4096, 4 * c->sms * 16), (c->K + kGatherThreads - 1) / kGatherThreads);
   if (c->partials && c->partials_cap >= need) return IPDG_OK;
   if (c->partials) cudaFree(c->partials);
   CUDA_TRY(c, cudaMalloc(&c->partials, 3 * sizeof(double) * need));

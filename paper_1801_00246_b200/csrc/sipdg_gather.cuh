@@ -17,6 +17,10 @@
 
 namespace ipdg {
 
+// threads per CTA of k_gather: small CTAs so register-heavy instantiations still fill an SM in steps
+// of 4 warps
+constexpr int kGatherThreads = 128;
+
 // neighbour element `n` seen through its face FP: its values and traces sJ n.grad u (its own outward
 // normal) at the face nodes, in its own face order
 template <int N, int FP>
@@ -41,7 +45,7 @@ __device__ __forceinline__ void gather_face(const double (&un)[TrT<N>::NP], doub
 }
 
 template <int N, int MODE, bool LAM>
-__global__ void __launch_bounds__(256) k_gather(AxArgs a) {
+__global__ void __launch_bounds__(kGatherThreads) k_gather(AxArgs a) {
   using T = TrT<N>;
   constexpr int NP = T::NP, NFP = T::NFP;
   constexpr bool PCG = (MODE == MODE_PCG_A);
