@@ -119,7 +119,7 @@ namespace ipdg {
 // __constant__ memory (c_tpe), the neighbour face values read from L1/L2 (as k_gather) -- no shared
 // memory, no block barriers.  Same formulas as k_dgop.
 template <int N, bool DIV>
-__global__ void __launch_bounds__(256) k_dgop_tpe(int64_t K, const double* __restrict__ f0, const double* __restrict__ f1,
+__global__ void __launch_bounds__(128) k_dgop_tpe(int64_t K, const double* __restrict__ f0, const double* __restrict__ f1,
                                                   const double4* __restrict__ geo, const int4* __restrict__ nbg,
                                                   double* __restrict__ o0, double* __restrict__ o1) {
   using T = TrT<N>;

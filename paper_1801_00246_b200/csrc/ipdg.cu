@@ -724,9 +724,9 @@ struct Impl {
   // DG gradient (div = false: o0, o1 = G p) or divergence (div = true: o0 = D u) with central fluxes
   static int dgop(ipdg_ctx c, bool div, const double* f0, const double* f1, double* o0, double* o1, cudaStream_t s) {
     if constexpr (N <= 4) {  // thread per element, operators in constant memory
-      const int grid = (int)std::max<int64_t>(1, (c->K + 255) / 256);
-      if (div) k_dgop_tpe<N, true><<<grid, 256, 0, s>>>(c->K, f0, f1, c->geo, c->nbg, o0, nullptr);
-      else k_dgop_tpe<N, false><<<grid, 256, 0, s>>>(c->K, f0, nullptr, c->geo, c->nbg, o0, o1);
+      const int grid = (int)std::max<int64_t>(1, (c->K + 127) / 128);  // 128-thread CTAs (register-heavy)
+      if (div) k_dgop_tpe<N, true><<<grid, 128, 0, s>>>(c->K, f0, f1, c->geo, c->nbg, o0, nullptr);
+      else k_dgop_tpe<N, false><<<grid, 128, 0, s>>>(c->K, f0, nullptr, c->geo, c->nbg, o0, o1);
       c->launches++;
       CUDA_TRY(c, cudaGetLastError());
       return IPDG_OK;
