@@ -13,6 +13,11 @@ module only marshals arguments.  PyTorch supplies device memory and streams
     u = torch.rand(op.K, op.Np, dtype=torch.float64, device="cuda")
     Au = op.ax(u)                                     # ipdg_ax
     x, stats = op.pcg_solve(b, tol=1e-8, maxit=5000)  # ipdg_pcg_solve (Jacobi by default)
+    x, stats = op.pcg_solve(b, lam=1e3, precond=2)     # screened Poisson, block-Jacobi
+    gx, gy = op.dg_grad(p); d = op.dg_div(ux, uy)       # DG gradient / divergence
+
+Preconditioners (``precond``): 0 none, 1 point Jacobi diag(A), 2 block-Jacobi scaled inverse
+mass (lambda > 0).
 """
 import ctypes
 
