@@ -163,3 +163,29 @@ def test_split_pass_a_two_launch_reduction(N):
     assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
     r = b.ravel() - A @ x.cpu().numpy().ravel()
     assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b) * 1.01
+
+
+def test_c4_recipe_small_cylinder():
+    """BASELINE config C4 recipe at a small size (the channel with the square cylinder, graded, outflow
+    Dirichlet, inflow / walls / cylinder Neumann, f = exp(-((x-2)^2 + y^2)/4)): Ax parity at N = 6 and
+    the Jacobi-PCG solve at N = 3 against the oracle (~4000 iterations: count within DESIGN.md R15,
+    solution held to the oracle's residual)."""
+    m = meshgen.cylinder(h0=0.1, ratio=1.3)
+    ref6 = RefElem(6)
+    A6 = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref6)
+    op6 = Ipdg(6, m)
+    u = meshgen.uniform_field(op6.K, op6.Np, seed=606)
+    Au = op6.ax(gpu(u)).cpu().numpy().ravel()
+    ref = A6 @ u.ravel()
+    assert np.linalg.norm(Au - ref) <= 1e-12 * np.linalg.norm(ref)
+    f = lambda x, y: np.exp(-((x - 2) ** 2 + y ** 2) / 4)  # noqa: E731
+    ref3 = RefElem(3)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref3)
+    b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref3, f)
+    op = Ipdg(3, m)
+    x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-8, maxit=20000)
+    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-8, 20000, dinv=1.0 / A.diagonal())
+    assert st["status"] == sto["status"] == 0
+    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    r = b.ravel() - A @ x.cpu().numpy().ravel()
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b) * 1.05
