@@ -83,6 +83,7 @@ class Ipdg:
             ro = np.ascontiguousarray(rm.recv_off, dtype=np.int64)
             check(lib().ipdg_upload_halo(op.ctx, rm.H, ge.ctypes.data, rem.ctypes.data, rf.ctypes.data, nr.size,
                                          nr.ctypes.data, so.ctypes.data, se.ctypes.data, ro.ctypes.data), op.ctx)
+            op._ws = None  # the library dropped the workspace binding (its layout depends on K + H)
         op.rank_mesh = rm
         return op
 
@@ -210,6 +211,7 @@ class Ipdg:
 
     def pcg_solve_host(self, b_host, x_host, lam=0.0, precond=1, tol=1e-8, maxit=10000, stream=None):
         """e2e path: host (pinned) numpy/torch CPU buffers in and out."""
+        self._workspace()
         st = ipdg_stats()
         rc = lib().ipdg_pcg_solve_host(self.ctx, ctypes.c_void_p(b_host.data_ptr()), ctypes.c_void_p(x_host.data_ptr()),
                                        float(lam), int(precond), float(tol), int(maxit), ctypes.byref(st),
@@ -247,9 +249,17 @@ class Ipdg:
         return dict(zip(keys, list(out)))
 
     def set_variant(self, variant):
-        """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux), 3 thread-per-element (k_tpe, N <= 4),
-        4 pipelined fused (k_pipe), 5 gather (k_gather, N <= 4)."""
+        """0 auto, 1 fused (k_sipdg), 2 split (k_grad + k_flux), 4 pipelined fused (k_pipe),
+        5 gather (k_gather, N <= 4)."""
         check(lib().ipdg_set_variant(self.ctx, int(variant)), self.ctx)
+
+    def debug_grid_cap(self, cap):
+        """Test hook (not in ipdg.h): cap every persistent grid at `cap` CTAs (0 = off), so a small mesh
+        runs several element blocks per CTA through the kernels' prefetch pipelines."""
+        fn = lib().ipdg_debug_grid_cap
+        fn.restype = ctypes.c_int
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        check(fn(self.ctx, int(cap)), self.ctx)
 
     def launch_count(self):
         return int(lib().ipdg_launch_count(self.ctx))

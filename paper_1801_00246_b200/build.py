@@ -1,4 +1,5 @@
 """Build libipdg.so in-tree for sm_100a (nvcc; no GPU needed)."""
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -9,8 +10,10 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libipdg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["ipdg.cu", "refops.cpp"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+# one translation unit per degree (impl_N.cu: the kernels of degree N and their dispatch), compiled in
+# parallel, then linked into one shared library
+SOURCES = ["ipdg.cu", "refops.cpp"] + ["impl_%d.cu" % n for n in range(1, 9)]
 
 
 def nccl_flags():
@@ -30,6 +33,7 @@ def nccl_flags():
 DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
+
 def _stale():
     if not os.path.exists(OUT):
         return True
@@ -38,18 +42,37 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in paths)
 
 
-def build_library(force=False, verbose=False):
+def build_library(force=False, verbose=False, extra=()):
+    extra = list(extra)
     if not force and not _stale():
         return OUT
     inc, link = nccl_flags()
-    cmd = [NVCC] + FLAGS + inc + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp"] + link
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    jobs = []
+    for s in SOURCES:  # largest degrees first: they take longest
+        obj = os.path.join(objdir, s.rsplit(".", 1)[0] + ".o")
+        cmd = [NVCC] + FLAGS + inc + extra + ["-c", os.path.join(CSRC, s), "-o", obj]
+        jobs.append((s, obj, cmd))
+    jobs.sort(key=lambda j: -int(j[0][5]) if j[0].startswith("impl_") else 0)
     log = os.path.join(HERE, "csrc", "ptxas_info.txt")
+    outs = []
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for (s, obj, cmd), res in zip(jobs, ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs)):
+            outs.append("==== %s\n%s%s" % (s, res.stdout, res.stderr))
+            if res.returncode != 0:
+                with open(log, "w") as f:
+                    f.write("".join(outs))
+                sys.stderr.write(res.stderr[-4000:])
+                raise RuntimeError("nvcc failed on %s (see %s)" % (s, log))
     with open(log, "w") as f:
-        f.write(res.stdout + res.stderr)
+        f.write("".join(outs))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC"] + \
+        [j[1] for j in jobs] + ["-o", OUT + ".tmp"] + link
+    res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-4000:])
-        raise RuntimeError("nvcc failed building libipdg.so (see %s)" % log)
+        raise RuntimeError("nvcc link of libipdg.so failed")
     os.replace(OUT + ".tmp", OUT)
     if verbose:
         print("built", OUT)

@@ -111,7 +111,7 @@ constexpr int dgop_smem_doubles() {
 
 }  // namespace ipdg
 
-#include "sipdg_tpe.cuh"
+#include "cops.cuh"
 
 namespace ipdg {
 

@@ -1,0 +1,3 @@
+// Degree-3 instantiation of the kernels and their host dispatch (impl.cuh).
+#include "impl.cuh"
+IPDG_DEFINE_OPS(3)

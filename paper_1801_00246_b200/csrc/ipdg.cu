@@ -17,765 +17,30 @@
 //           pass B (k_pcg_b): alpha_k = rho_{k-1}/red_A (breakdown if <= 0);
 //             r -= alpha_k Ap; red_B = (r.z, r.r); it = k               [+ allreduce(2)]
 //   end:    pending x += alpha_k p_k if no stop was decided; stats to host.
-#include <cuda_runtime.h>
-#include <nccl.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <numeric>
-#include <string>
-#include <vector>
-
-#include "../../include/ipdg.h"
-#include "refops.h"
+#include "ctx.h"
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
-#include "sipdg_tpe.cuh"
 #include "sipdg_pipe.cuh"
-#include "pcg_blockjacobi.cuh"
-#include "sipdg_gather.cuh"
-#include "dgops.cuh"
 
-using namespace ipdg;
+#include <numeric>
 
-struct ipdg_ctx_s {
-  int N = 0, device = 0, sms = 0;
-  RefOps ref;
-  int64_t K = 0, H = 0;  // local elements, halo ghosts
-  double tau_c = 0.0;
-  bool has_dirichlet = false;
-  // device mesh data
-  double4* geo = nullptr;
-  double4* gG = nullptr;  // per-element J G^T G records (k_pipe)
-  double* gF = nullptr;   // per-face lift coefficients and sJ tau (k_pipe)
-  short4* nbr = nullptr;
-  int* goff = nullptr;
-  int* gid = nullptr;
-  int* boff = nullptr;
-  int* etoe = nullptr;
-  int8_t* bcode = nullptr;
-  double* vxy = nullptr;
-  double* rs = nullptr;
-  double* Mref = nullptr;
-  double* Minv = nullptr;  // M^{-1} (block-Jacobi preconditioner)
-  double* dgops = nullptr; // Dr | Ds | LIFT (DG gradient / divergence)
-  double* tables = nullptr;
-  double* diagtab = nullptr;
-  int nblocks = 0, gmax = 0;
-  int E = 0;
-  // split variant (k_grad + k_flux): neighbour ids per element, W = [w_r | w_s] scratch
-  int4* nbg = nullptr;
-  double* W2 = nullptr;
-  int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4), 4 pipelined fused
-  // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit
-  size_t smem_pipe[2][2] = {{0, 0}, {0, 0}};
-  int grid_pipe[2][2] = {{0, 0}, {0, 0}};
-  bool pipe_xb[2] = {false, false};  // [lam]: k_pipe's pass A leaves x to pass B (no room for x staging)
-  // thread-per-element variant (k_tpe): its own block schedule
-  int t_nblocks = 0;
-  int *t_boff = nullptr, *t_goff = nullptr, *t_gid = nullptr;
-  short4* t_nbr = nullptr;
-  size_t smem_tpe[2] = {0, 0};
-  int grid_tpe[2][2] = {{0, 0}, {0, 0}};
-  size_t smem_grad = 0, smem_flux[2] = {0, 0};
-  int grid_grad = 0, grid_flux[2][2] = {{0, 0}, {0, 0}};
-  size_t smem[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
-  int grid[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]
-  // host copies for introspection
-  std::vector<int> etoe_h, etof_h;
-  // PCG
-  PcgState* st = nullptr;
-  PcgState* st_host = nullptr;
-  double* partials = nullptr;
-  int partials_cap = 0;  // slots per reduced quantity
-  unsigned int* counter = nullptr;
-  void* ws = nullptr;
-  int64_t ws_bytes = 0;
-  bool ws_owned = false;
-  double *r = nullptr, *pe = nullptr, *po = nullptr, *Ap = nullptr, *dinv = nullptr, *zb = nullptr;
-  double dinv_lambda = -1.0;
-  bool dinv_valid = false;
-  // current solve
-  double* x = nullptr;
-  double lambda = 0.0;
-  int precond = 0;
-  bool xb = false;  // pass B updates x (k_pipe pass A); else pass A applies the deferred update
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // [0]: 1 iteration, [1]: kChunk iterations
-  const void* gkey_x = nullptr;
-  double gkey_lambda = -1.0;
-  int gkey_precond = -1;
-  cudaStream_t cap_stream = nullptr;
-  // split pass A (k_pipe): interior blocks, then halo-boundary blocks once the exchange (on comm_stream)
-  // has landed -- the halo exchange overlaps the interior work
-  bool split_a = false;        // multi-GPU halo, or forced for tests (ipdg_debug_split_pass_a)
-  int force_split = 0;
-  int* blist = nullptr;        // [interior block ids | boundary block ids]
-  int nb_split[2] = {0, 0};
-  cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
-  bool halo_ev_pending = false;
-  // pending host mesh (ipdg_upload_mesh -> ipdg_upload_halo)
-  int64_t pend_K = 0, pend_remote = 0;
-  std::vector<int> pend_etoe, pend_etof;
-  std::vector<int8_t> pend_bc;
-  std::vector<double> pend_vxy, pend_VX, pend_VY;
-  // halo (multi-GPU): S sent element rows, H received ghost rows
-  int64_t S = 0;
-  int* send_idx = nullptr;
-  double* sendbuf = nullptr;
-  double* halobuf = nullptr;
-  std::vector<int> nbr_rank;
-  std::vector<int64_t> send_off, recv_off;
-  bool has_dirichlet_global = false;
-  bool halo_external = false;  // caller fills the halo buffer (ipdg_halo_set), no NCCL
-  // multi-GPU
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0;
-  std::string err;
-  int64_t launches = 0;
-  int launches_per_iter = 2;  // kernels per PCG iteration (set when the iteration graph is captured)
-};
 
-static constexpr int kChunk = 32;
-static constexpr int kCommSlots = 8;  // CTA slots left free for NCCL during an overlapped pass
+#define IPDG_DECL_OPS(N_) const ImplOps* impl_ops_##N_();
+IPDG_DECL_OPS(1) IPDG_DECL_OPS(2) IPDG_DECL_OPS(3) IPDG_DECL_OPS(4)
+IPDG_DECL_OPS(5) IPDG_DECL_OPS(6) IPDG_DECL_OPS(7) IPDG_DECL_OPS(8)
+const ImplOps* impl_ops(int N) {
+  switch (N) {
+    case 1: return impl_ops_1(); case 2: return impl_ops_2(); case 3: return impl_ops_3(); case 4: return impl_ops_4();
+    case 5: return impl_ops_5(); case 6: return impl_ops_6(); case 7: return impl_ops_7(); default: return impl_ops_8();
+  }
+}
 
-#define FAIL(ctx, code, ...)                                         \
-  do {                                                              \
-    char b_[512];                                                   \
-    snprintf(b_, sizeof(b_), __VA_ARGS__);                          \
-    if (ctx) (ctx)->err = b_;                                        \
-    return code;                                                    \
+
+#define DISPATCH(N_, CALL)                          \
+  do {                                              \
+    if ((N_) < 1 || (N_) > 8) return IPDG_EDEGREE;  \
+    return impl_ops(N_)->CALL;                      \
   } while (0)
-#define CUDA_TRY(ctx, x)                                                                            \
-  do {                                                                                             \
-    cudaError_t e_ = (x);                                                                          \
-    if (e_ != cudaSuccess) FAIL(ctx, IPDG_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-#define NCCL_TRY(ctx, x)                                                                           \
-  do {                                                                                             \
-    ncclResult_t r_ = (x);                                                                         \
-    if (r_ != ncclSuccess) FAIL(ctx, IPDG_ENCCL, "%s: %s", #x, ncclGetErrorString(r_));            \
-  } while (0)
-
-#define TRY(x)                 \
-  do {                         \
-    int rc_ = (x);             \
-    if (rc_ != IPDG_OK) return rc_; \
-  } while (0)
-
-// ------------------------------------------------------------------ per-N dispatch
-template <int N>
-struct Impl {
-  using T = Tr<N>;
-
-  // DMMA fragment tables: [chunk][ntile][lane], lane -> (k = lane & 3, n = lane >> 2)
-  static std::vector<double> build_tables(const RefOps& R) {
-    const int NP = T::NP, NFP = T::NFP, NF3 = T::NF3, NT = T::NT;
-    std::vector<double> tab(T::TAB_G + T::TAB_M + T::TAB_L, 0.0);
-    double* tg = tab.data();
-    double* tm = tg + T::TAB_G;
-    double* tl = tm + T::TAB_M;
-    auto at = [&](const std::vector<double>& A, int ld, int i, int j, int ni, int nj) {
-      return (i < ni && j < nj) ? A[i * ld + j] : 0.0;
-    };
-    for (int kc = 0; kc < T::KCG; ++kc)
-      for (int q = 0; q < 2 * NT; ++q)
-        for (int l = 0; l < 32; ++l) {
-          const int k = 4 * kc + (l & 3), n = 8 * (q % NT) + (l >> 2);
-          const std::vector<double>& D = (q < NT) ? R.Dr : R.Ds;
-          tg[(kc * 2 * NT + q) * 32 + l] = at(D, NP, n, k, NP, NP);  // B[k][n] = D[n][k]
-        }
-    // LIFT^T Sr, LIFT^T Ss  (3Nfp x Np)
-    std::vector<double> LSr(NF3 * NP, 0.0), LSs(NF3 * NP, 0.0);
-    for (int m = 0; m < NF3; ++m)
-      for (int n = 0; n < NP; ++n) {
-        double a = 0, b = 0;
-        for (int i = 0; i < NP; ++i) {
-          a += R.LIFT[i * NF3 + m] * R.Sr[i * NP + n];
-          b += R.LIFT[i * NF3 + m] * R.Ss[i * NP + n];
-        }
-        LSr[m * NP + n] = a;
-        LSs[m * NP + n] = b;
-      }
-    for (int c = 0; c < T::KCW + T::KCF; ++c)
-      for (int j = 0; j < NT; ++j)
-        for (int l = 0; l < 32; ++l) {
-          const int n = 8 * j + (l >> 2);
-          double v = 0.0;
-          if (c < 4 * NT) {  // w_r / w_s chunks straight from the C-fragment layout
-            const int cc = c % (2 * NT);
-            const int i = 8 * (cc >> 1) + 2 * (l & 3) + (cc & 1);
-            v = at(c < 2 * NT ? R.Sr : R.Ss, NP, i, n, NP, NP);
-          } else {
-            const int m = 4 * (c - 4 * NT) + (l & 3);
-            const int blk = m / T::NF3P, mm = m % T::NF3P;  // three face sub-blocks, each padded to NF3P
-            if (mm >= NF3) v = 0.0;
-            else if (blk == 0) v = at(LSr, NP, mm, n, NF3, NP);
-            else if (blk == 1) v = at(LSs, NP, mm, n, NF3, NP);
-            else {  // face mass scattered to the face rows: E[n][m'] (E = M LIFT)
-              const int f = mm / NFP, kk = mm % NFP;
-              if (n < NP)
-                for (int q = 0; q < NFP; ++q)
-                  if (R.Fmask[f * NFP + q] == n) v = R.M1D[q * NFP + kk];
-            }
-          }
-          tm[(c * NT + j) * 32 + l] = v;
-        }
-    for (int kc = 0; kc < T::KCM; ++kc)
-      for (int j = 0; j < NT; ++j)
-        for (int l = 0; l < 32; ++l) {
-          const int k = 4 * kc + (l & 3), n = 8 * j + (l >> 2);
-          tl[(kc * NT + j) * 32 + l] = at(R.M, NP, k, n, NP, NP);
-        }
-    // aux: M1D, then ints fmask[NF3], nodeface[2*NPN]
-    for (int i = 0; i < NFP * NFP; ++i) tab.push_back(R.M1D[i]);
-    std::vector<int> ia(NF3 + 2 * T::NPN, -1);
-    for (int i = 0; i < NF3; ++i) ia[i] = R.Fmask[i];
-    for (int f = 0; f < 3; ++f)
-      for (int k = 0; k < NFP; ++k) {
-        const int i = R.Fmask[f * NFP + k];
-        int* slot = &ia[NF3 + 2 * i];
-        if (slot[0] < 0) slot[0] = f * NFP + k;
-        else slot[1] = f * NFP + k;
-      }
-    if (ia.size() % 2) ia.push_back(-1);
-    const size_t base = tab.size();
-    tab.resize(base + ia.size() / 2);
-    std::memcpy(tab.data() + base, ia.data(), ia.size() * sizeof(int));
-    // split variant (k_flux): main table with w_r, w_s rows in natural node order
-    using S = TrS<N>;
-    tab.resize(S::OFF_M2, 0.0);
-    tm = tab.data() + T::TAB_G;  // the vector may have moved
-    std::vector<double> m2(S::TAB_M2, 0.0);
-    for (int c = 0; c < S::KCW2 + T::KCF; ++c)
-      for (int j = 0; j < NT; ++j)
-        for (int l = 0; l < 32; ++l) {
-          const int n = 8 * j + (l >> 2);
-          double v;
-          if (c < S::KCW2) {
-            const int k = 4 * (c % T::KCG) + (l & 3);
-            v = at(c < T::KCG ? R.Sr : R.Ss, NP, k, n, NP, NP);
-          } else {
-            v = tm[((c - S::KCW2 + T::KCW) * NT + j) * 32 + l];  // face chunks: same as the fused table
-          }
-          m2[(c * NT + j) * 32 + l] = v;
-        }
-    tab.insert(tab.end(), m2.begin(), m2.end());
-    return tab;
-  }
-
-  static std::vector<double> build_diagtab(const RefOps& R) {
-    const int NP = T::NP, NFP = T::NFP, NF3 = T::NF3;
-    std::vector<double> d(4 * NP + 2 * NF3 + NFP + NF3, 0.0);
-    for (int i = 0; i < NP; ++i) {
-      double krr = 0, krs = 0, kss = 0;
-      for (int a = 0; a < NP; ++a)
-        for (int b = 0; b < NP; ++b) {
-          const double m = R.M[a * NP + b];
-          krr += R.Dr[a * NP + i] * m * R.Dr[b * NP + i];
-          krs += R.Dr[a * NP + i] * m * R.Ds[b * NP + i];
-          kss += R.Ds[a * NP + i] * m * R.Ds[b * NP + i];
-        }
-      d[i] = krr;
-      d[NP + i] = krs;
-      d[2 * NP + i] = kss;
-      d[3 * NP + i] = R.M[i * NP + i];
-    }
-    for (int f = 0; f < 3; ++f)
-      for (int k = 0; k < NFP; ++k) {
-        const int i = R.Fmask[f * NFP + k];
-        double pr = 0, ps = 0;
-        for (int m = 0; m < NFP; ++m) {
-          const int fm = R.Fmask[f * NFP + m];
-          pr += R.Dr[fm * NP + i] * R.M1D[m * NFP + k];
-          ps += R.Ds[fm * NP + i] * R.M1D[m * NFP + k];
-        }
-        d[4 * NP + f * NFP + k] = pr;
-        d[4 * NP + NF3 + f * NFP + k] = ps;
-      }
-    for (int k = 0; k < NFP; ++k) d[4 * NP + 2 * NF3 + k] = R.M1D[k * NFP + k];
-    for (int i = 0; i < NF3; ++i) d[4 * NP + 2 * NF3 + NFP + i] = R.Fmask[i];
-    return d;
-  }
-
-  static int configure(ipdg_ctx c) {
-    int optin = 0;
-    CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    for (int lam = 0; lam < 2; ++lam) {
-      for (int mode = 0; mode < 2; ++mode) {
-        const SmemLayout L = SmemLayout::make<N>(c->gmax, lam != 0, mode == 1);
-        const size_t bytes = (size_t)L.total * sizeof(double);
-        c->smem[mode][lam] = bytes;
-        const void* fn = (mode == 0) ? (lam ? (const void*)k_sipdg<N, MODE_AX, true> : (const void*)k_sipdg<N, MODE_AX, false>)
-                                     : (lam ? (const void*)k_sipdg<N, MODE_PCG_A, true>
-                                            : (const void*)k_sipdg<N, MODE_PCG_A, false>);
-        // opt in to the full per-CTA maximum once: the attribute is per function (shared by all
-        // contexts of this N), the launch passes the context's own byte count
-        if ((int)bytes > optin - 1024) FAIL(c, IPDG_ECUDA, "k_sipdg<N=%d> needs %zu B of shared memory", N, bytes);
-        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        int occ = 0;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
-        if (occ < 1) FAIL(c, IPDG_ECUDA, "k_sipdg<N=%d> does not fit on an SM (smem %zu B, gmax %d)", N, bytes, c->gmax);
-        c->grid[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
-      }
-    }
-    // split variant
-    using S = TrS<N>;
-    {
-      const size_t bytes = (size_t)(T::TAB_G + S::W * 8 * T::SU) * sizeof(double);
-      c->smem_grad = bytes;
-      const void* fns[2] = {(const void*)k_grad<N, MODE_AX>, (const void*)k_grad<N, MODE_PCG_A>};
-      int occ = 1;
-      for (const void* fn : fns) {
-        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        int o = 0;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, S::W * 32, bytes));
-        occ = std::max(1, o);
-      }
-      const int64_t tiles = (c->K + c->H + 7) / 8;
-      c->grid_grad = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)occ * c->sms));
-    }
-    for (int lam = 0; lam < 2; ++lam) {
-      const size_t bytes = (size_t)(S::TAB_M2 + (lam ? T::TAB_L : 0)) * sizeof(double);
-      c->smem_flux[lam] = bytes;
-      for (int mode = 0; mode < 2; ++mode) {
-        const void* fn = (mode == 0) ? (lam ? (const void*)k_flux<N, MODE_AX, true> : (const void*)k_flux<N, MODE_AX, false>)
-                                     : (lam ? (const void*)k_flux<N, MODE_PCG_A, true> : (const void*)k_flux<N, MODE_PCG_A, false>);
-        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        int o = 0;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, S::W * 32, bytes));
-        const int64_t tiles = (c->K + 7) / 8;
-        c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
-      }
-    }
-    TRY(configure_pipe(c, optin));
-    return configure_tpe(c, optin);
-  }
-
-  // ---- pipelined fused variant: needs room for the staging area next to the working rows
-  static int configure_pipe(ipdg_ctx c, int optin) {
-    for (int lam = 0; lam < 2; ++lam)
-      for (int mode = 0; mode < 2; ++mode) {
-        const void* fn = (mode == 0) ? (lam ? (const void*)k_pipe<N, MODE_AX, true> : (const void*)k_pipe<N, MODE_AX, false>)
-                                     : (lam ? (const void*)k_pipe<N, MODE_PCG_A, true> : (const void*)k_pipe<N, MODE_PCG_A, false>);
-        c->grid_pipe[mode][lam] = 0;
-        c->pipe_xb[lam] = false;
-        int best = 0;
-        // PCG pass A: stage x for the deferred update unless that costs a resident CTA per SM, in which
-        // case pass B updates x (AxArgs::defer_x = 0)
-        for (int xs = 1; xs >= (mode == 1 ? 0 : 1); --xs) {
-          const PipeLayout L = PipeLayout::make<N>(c->gmax, lam != 0, mode == 1, xs != 0);
-          const size_t bytes = (size_t)L.total() * sizeof(double);
-          if ((int)bytes > optin - 1024) continue;
-          CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-          int occ = 0;
-          CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T::W * 32, bytes));
-          if (occ > best) {
-            best = occ;
-            c->smem_pipe[mode][lam] = bytes;
-            c->grid_pipe[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
-            if (mode == 1) c->pipe_xb[lam] = (xs == 0);
-          }
-        }
-      }
-    return IPDG_OK;
-  }
-
-  // ---- thread-per-element variant (N <= 4)
-  static int configure_tpe(ipdg_ctx c, int optin) {
-    if constexpr (N <= 4) {
-      using TT = TrT<N>;
-      for (int mode = 0; mode < 2; ++mode) {
-        const size_t bytes = (size_t)(mode == 1 ? TpeSmem<N, true>::total() : TpeSmem<N, false>::total()) * sizeof(double);
-        c->smem_tpe[mode] = bytes;
-        for (int lam = 0; lam < 2; ++lam) {
-          const void* fn = (mode == 0) ? (lam ? (const void*)k_tpe<N, MODE_AX, true> : (const void*)k_tpe<N, MODE_AX, false>)
-                                       : (lam ? (const void*)k_tpe<N, MODE_PCG_A, true> : (const void*)k_tpe<N, MODE_PCG_A, false>);
-          CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-          int o = 0;
-          CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, TT::NTHR, bytes));
-          c->grid_tpe[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>(c->t_nblocks, (int64_t)std::max(1, o) * c->sms));
-        }
-      }
-    }
-    return IPDG_OK;
-  }
-
-  static int upload_tpe_constants(ipdg_ctx c) {
-    if constexpr (N <= 4) {
-      using TT = TrT<N>;
-      const RefOps& R = c->ref;
-      const int NP = TT::NP, NFP = TT::NFP, NF3 = TT::NF3;
-      std::vector<double> h(TT::TOTAL, 0.0);
-      for (int i = 0; i < NP * NP; ++i) {
-        h[TT::O_DR + i] = R.Dr[i];
-        h[TT::O_DS + i] = R.Ds[i];
-        h[TT::O_SR + i] = R.Sr[i];
-        h[TT::O_SS + i] = R.Ss[i];
-        h[TT::O_M + i] = R.M[i];
-      }
-      for (int m = 0; m < NF3; ++m)
-        for (int n = 0; n < NP; ++n) {
-          double a = 0, b = 0;
-          for (int i = 0; i < NP; ++i) {
-            a += R.LIFT[i * NF3 + m] * R.Sr[i * NP + n];
-            b += R.LIFT[i * NF3 + m] * R.Ss[i * NP + n];
-          }
-          h[TT::O_LSR + m * NP + n] = a;
-          h[TT::O_LSS + m * NP + n] = b;
-        }
-      for (int i = 0; i < NFP * NFP; ++i) h[TT::O_M1D + i] = R.M1D[i];
-      for (int i = 0; i < NP * NF3; ++i) h[TT::O_LIFT + i] = R.LIFT[i];
-      CUDA_TRY(c, cudaMemcpyToSymbol(c_tpe<N>, h.data(), h.size() * sizeof(double)));
-    }
-    return IPDG_OK;
-  }
-
-  static TpeArgs targs(ipdg_ctx c) {
-    TpeArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.K = c->K;
-    a.nblocks = c->t_nblocks;
-    a.boff = c->t_boff;
-    a.goff = c->t_goff;
-    a.gid = c->t_gid;
-    a.nbr = c->t_nbr;
-    a.geo = c->geo;
-    a.tau_c = c->tau_c;
-    a.halo = c->halobuf;
-    return a;
-  }
-
-  static int ax_tpe(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
-    if constexpr (N <= 4) {
-      TpeArgs a = targs(c);
-      a.u = u;
-      a.Au = Au;
-      a.lambda = lambda;
-      if (lambda != 0.0) k_tpe<N, MODE_AX, true><<<c->grid_tpe[0][1], TrT<N>::NTHR, c->smem_tpe[0], s>>>(a);
-      else k_tpe<N, MODE_AX, false><<<c->grid_tpe[0][0], TrT<N>::NTHR, c->smem_tpe[0], s>>>(a);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
-    } else {
-      FAIL(c, IPDG_EINVAL, "thread-per-element variant needs N <= 4");
-    }
-  }
-
-  static int pass_a_tpe(ipdg_ctx c, cudaStream_t s) {
-    if constexpr (N <= 4) {
-      TpeArgs a = targs(c);
-      a.lambda = c->lambda;
-      a.z = c->precond ? c->zb : c->r;
-      a.p_even = c->pe;
-      a.p_odd = c->po;
-      a.x = c->x;
-      a.Au = c->Ap;
-      a.st = c->st;
-      a.partials = c->partials;
-      a.counter = c->counter;
-      if (c->lambda != 0.0) k_tpe<N, MODE_PCG_A, true><<<c->grid_tpe[1][1], TrT<N>::NTHR, c->smem_tpe[1], s>>>(a);
-      else k_tpe<N, MODE_PCG_A, false><<<c->grid_tpe[1][0], TrT<N>::NTHR, c->smem_tpe[1], s>>>(a);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
-    } else {
-      FAIL(c, IPDG_EINVAL, "thread-per-element variant needs N <= 4");
-    }
-  }
-
-  // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
-  static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
-  // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe, 5 gather).
-  // Auto (variant 0), the fastest measured per degree and pass: Ax -- gather for N <= 3, pipelined fused
-  // for N = 4, 5, split for N >= 6 (C3 sweep, profiles/r01_sweep_*.jsonl); PCG pass A -- gather for N = 1,
-  // pipelined fused for N = 2..5 (its p formation and x update are cheaper in the staged kernel:
-  // tools/pcg_lowN_timing.py on C2, N = 2: 47 vs 50 us, N = 3: 68 vs 74 us), split for N >= 6.
-  // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
-  static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
-    int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : (N <= (mode == 0 ? 3 : 1) ? 5 : 4);
-    if ((k == 3 || k == 5) && N > 4) k = 1;
-    if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
-    return k;
-  }
-
-  // gather variant (N <= 4): one thread per element, grid-stride
-  template <int MODE>
-  static int launch_gather(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s) {
-    if constexpr (N <= 4) {
-      const int grid = (int)std::max<int64_t>(1, (c->K + kGatherThreads - 1) / kGatherThreads);  // one element per thread
-      if (MODE == MODE_PCG_A && grid > c->partials_cap) FAIL(c, IPDG_ECUDA, "partials buffer too small");
-      if (lam) k_gather<N, MODE, true><<<grid, kGatherThreads, 0, s>>>(a);
-      else k_gather<N, MODE, false><<<grid, kGatherThreads, 0, s>>>(a);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
-    } else {
-      FAIL(c, IPDG_EINVAL, "gather variant needs N <= 4");
-    }
-  }
-
-  static SplitArgs sargs(ipdg_ctx c) {
-    SplitArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.K = c->K;
-    a.H = c->H;
-    a.geo = c->geo;
-    a.nbg = c->nbg;
-    a.tables = c->tables;
-    a.tau_c = c->tau_c;
-    a.halo = c->halobuf;
-    a.W2 = c->W2;
-    a.gG = c->gG;
-    a.gF = c->gF;
-    a.ebeg = 0;
-    a.eend = c->K + c->H;
-    a.stop_work = 1;
-    return a;
-  }
-
-  // k_grad over [K, K + H) alone: the halo rows, once the exchange has landed
-  static int grad_launch(ipdg_ctx c, SplitArgs a, int mode, int64_t ebeg, int64_t eend, int stop_work, cudaStream_t s,
-                         int spare = 0) {
-    using S = TrS<N>;
-    a.ebeg = ebeg;
-    a.eend = eend;
-    a.stop_work = stop_work;
-    const int64_t tiles = std::max<int64_t>(1, (eend - ebeg + 7) / 8);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)c->grid_grad - spare));
-    if (mode == 0) k_grad<N, MODE_AX><<<g, S::W * 32, c->smem_grad, s>>>(a);
-    else k_grad<N, MODE_PCG_A><<<g, S::W * 32, c->smem_grad, s>>>(a);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static int ensure_w2(ipdg_ctx c) {
-    if (c->W2) return IPDG_OK;
-    CUDA_TRY(c, cudaMalloc(&c->W2, std::max<int64_t>(1, c->K + c->H) * 2 * T::NP * sizeof(double)));
-    return IPDG_OK;
-  }
-
-  static int ax_split(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
-    TRY(ensure_w2(c));
-    SplitArgs a = sargs(c);
-    a.W2 = c->W2;
-    a.u = u;
-    a.Au = Au;
-    a.lambda = lambda;
-    using S = TrS<N>;
-    if (c->H > 0) {  // own rows, then halo rows (the same split as the overlapped PCG pass A)
-      TRY(grad_launch(c, a, 0, 0, c->K, 1, s));
-      TRY(grad_launch(c, a, 0, c->K, c->K + c->H, 0, s));
-    } else {
-      k_grad<N, MODE_AX><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
-      c->launches++;
-    }
-    if (lambda != 0.0) k_flux<N, MODE_AX, true><<<c->grid_flux[0][1], S::W * 32, c->smem_flux[1], s>>>(a);
-    else k_flux<N, MODE_AX, false><<<c->grid_flux[0][0], S::W * 32, c->smem_flux[0], s>>>(a);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static int pass_a_split(ipdg_ctx c, cudaStream_t s) {
-    TRY(ensure_w2(c));
-    SplitArgs a = sargs(c);
-    a.W2 = c->W2;
-    a.lambda = c->lambda;
-    a.z = c->precond ? c->zb : c->r;
-    a.p_even = c->pe;
-    a.p_odd = c->po;
-    a.x = c->x;
-    a.Au = c->Ap;
-    a.st = c->st;
-    a.partials = c->partials;
-    a.counter = c->counter;
-    using S = TrS<N>;
-    if (c->H > 0) {  // own rows overlap the halo exchange (comm stream); halo rows once it has landed
-      TRY(grad_launch(c, a, 1, 0, c->K, 1, s, c->halo_ev_pending ? kCommSlots : 0));
-      if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
-      TRY(grad_launch(c, a, 1, c->K, c->K + c->H, 0, s));
-    } else {
-      k_grad<N, MODE_PCG_A><<<c->grid_grad, S::W * 32, c->smem_grad, s>>>(a);
-      c->launches++;
-    }
-    if (c->lambda != 0.0) k_flux<N, MODE_PCG_A, true><<<c->grid_flux[1][1], S::W * 32, c->smem_flux[1], s>>>(a);
-    else k_flux<N, MODE_PCG_A, false><<<c->grid_flux[1][0], S::W * 32, c->smem_flux[0], s>>>(a);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static AxArgs args(ipdg_ctx c) {
-    AxArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.K = c->K;
-    a.H = c->H;
-    a.nblocks = c->nblocks;
-    a.geo = c->geo;
-    a.nbr = c->nbr;
-    a.goff = c->goff;
-    a.gid = c->gid;
-    a.boff = c->boff;
-    a.tables = c->tables;
-    a.gG = c->gG;
-    a.gF = c->gF;
-    a.nbg = c->nbg;
-    a.tau_c = c->tau_c;
-    a.halo_p = c->halobuf;
-    return a;
-  }
-
-  static int ax(ipdg_ctx c, const double* u, double* Au, double lambda, cudaStream_t s) {
-    const bool lam = lambda != 0.0;
-    const int k = resolve(c, 0, lam, u);
-    if (k == 3) return ax_tpe(c, u, Au, lambda, s);
-    if (k == 2) return ax_split(c, u, Au, lambda, s);
-    AxArgs a = args(c);
-    a.u = u;
-    a.Au = Au;
-    a.lambda = lambda;
-    if (k == 5) return launch_gather<MODE_AX>(c, a, lam, s);
-    if (k == 4) {
-      const int gp = c->grid_pipe[0][lam];
-      if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
-      else k_pipe<N, MODE_AX, false><<<gp, T::W * 32, c->smem_pipe[0][0], s>>>(a, c->gmax);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
-    }
-    const int g = c->grid[0][lam];
-    if (lam) k_sipdg<N, MODE_AX, true><<<g, T::W * 32, c->smem[0][1], s>>>(a, c->gmax);
-    else k_sipdg<N, MODE_AX, false><<<g, T::W * 32, c->smem[0][0], s>>>(a, c->gmax);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static int pass_a(ipdg_ctx c, cudaStream_t s) {
-    const int k = resolve(c, 1, c->lambda != 0.0, c->x);
-    if (k == 3) return pass_a_tpe(c, s);
-    if (k == 2) return pass_a_split(c, s);
-    AxArgs a = args(c);
-    a.lambda = c->lambda;
-    a.r = c->r;
-    a.dinv = c->precond ? c->dinv : nullptr;
-    a.z = c->precond ? c->zb : c->r;
-    a.p_even = c->pe;
-    a.p_odd = c->po;
-    a.x = c->x;
-    a.defer_x = c->xb ? 0 : 1;
-    a.Au = c->Ap;
-    a.st = c->st;
-    a.partials = c->partials;
-    a.counter = c->counter;
-    const bool lam = c->lambda != 0.0;
-    if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
-    if (k == 4) {
-      const int gp = c->grid_pipe[1][lam];
-      auto launch = [&](int part, const int* list, int n) -> int {
-        a.blist = list;
-        a.nlist = n;
-        a.red_part = part;
-        // while the exchange is in flight leave a few CTA slots free for NCCL's kernel (the persistent grid
-        // would otherwise fill every SM and the exchange could only start after the interior blocks)
-        const int cap = (part == 1 && c->halo_ev_pending) ? std::max(1, gp - kCommSlots) : gp;
-        const int g = list ? std::max(1, std::min(cap, n)) : gp;
-        if (lam) k_pipe<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem_pipe[1][1], s>>>(a, c->gmax);
-        else k_pipe<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem_pipe[1][0], s>>>(a, c->gmax);
-        c->launches++;
-        CUDA_TRY(c, cudaGetLastError());
-        return IPDG_OK;
-      };
-      if (c->split_a) {  // interior blocks, (wait for the halo exchange), halo-boundary blocks
-        TRY(launch(1, c->blist, c->nb_split[0]));
-        if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
-        return launch(2, c->blist + c->nb_split[0], c->nb_split[1]);
-      }
-      return launch(0, nullptr, 0);
-    }
-    const int g = c->grid[1][lam];
-    if (lam) k_sipdg<N, MODE_PCG_A, true><<<g, T::W * 32, c->smem[1][1], s>>>(a, c->gmax);
-    else k_sipdg<N, MODE_PCG_A, false><<<g, T::W * 32, c->smem[1][0], s>>>(a, c->gmax);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  // block-Jacobi (scaled inverse mass) residual pass: init (r = b - Ax0) or update (r -= alpha Ap)
-  static int pass_b_bj(ipdg_ctx c, bool init, const double* b, cudaStream_t s) {
-    constexpr int EPB = 256 / T::NP;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->K + EPB - 1) / EPB, (int64_t)c->sms * 8));
-    if (init)
-      k_pcg_bj<N, true><<<grid, 256, 0, s>>>(c->K, b, c->Ap, c->r, c->zb, c->gG, c->Minv, c->lambda, c->st, c->partials,
-                                             c->counter, nullptr, nullptr, nullptr);
-    else
-      k_pcg_bj<N, false><<<grid, 256, 0, s>>>(c->K, c->r, c->Ap, c->r, c->zb, c->gG, c->Minv, c->lambda, c->st,
-                                              c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  // DG gradient (div = false: o0, o1 = G p) or divergence (div = true: o0 = D u) with central fluxes
-  static int dgop(ipdg_ctx c, bool div, const double* f0, const double* f1, double* o0, double* o1, cudaStream_t s) {
-    if constexpr (N <= 4) {  // thread per element, operators in constant memory
-      const int grid = (int)std::max<int64_t>(1, (c->K + 127) / 128);  // 128-thread CTAs (register-heavy)
-      if (div) k_dgop_tpe<N, true><<<grid, 128, 0, s>>>(c->K, f0, f1, c->geo, c->nbg, o0, nullptr);
-      else k_dgop_tpe<N, false><<<grid, 128, 0, s>>>(c->K, f0, nullptr, c->geo, c->nbg, o0, o1);
-      c->launches++;
-      CUDA_TRY(c, cudaGetLastError());
-      return IPDG_OK;
-    }
-    constexpr int EPB = 256 / T::NP;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->K + EPB - 1) / EPB, (int64_t)c->sms * 8));
-    if (div) {
-      constexpr size_t bytes = dgop_smem_doubles<N, true>() * sizeof(double);
-      CUDA_TRY(c, cudaFuncSetAttribute(k_dgop<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      k_dgop<N, true><<<grid, 256, bytes, s>>>(c->K, f0, f1, c->geo, c->nbg, c->dgops, o0, nullptr);
-    } else {
-      constexpr size_t bytes = dgop_smem_doubles<N, false>() * sizeof(double);
-      CUDA_TRY(c, cudaFuncSetAttribute(k_dgop<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      k_dgop<N, false><<<grid, 256, bytes, s>>>(c->K, f0, nullptr, c->geo, c->nbg, c->dgops, o0, o1);
-    }
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static int diag(ipdg_ctx c, double* d, double lambda, cudaStream_t s) {
-    const int64_t n = c->K * T::NP;
-    k_diag<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->etoe, c->bcode, c->diagtab, c->tau_c, lambda, d);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-
-  static int mass(ipdg_ctx c, const double* u, double* Mu, cudaStream_t s) {
-    const int64_t n = c->K * T::NP;
-    k_mass<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->Mref, u, Mu);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-    return IPDG_OK;
-  }
-};
-
-#define DISPATCH(N_, CALL)                     \
-  switch (N_) {                                \
-    case 1: return Impl<1>::CALL;              \
-    case 2: return Impl<2>::CALL;              \
-    case 3: return Impl<3>::CALL;              \
-    case 4: return Impl<4>::CALL;              \
-    case 5: return Impl<5>::CALL;              \
-    case 6: return Impl<6>::CALL;              \
-    case 7: return Impl<7>::CALL;              \
-    case 8: return Impl<8>::CALL;              \
-    default: return IPDG_EDEGREE;              \
-  }
 
 static int e_of(int N) {
   switch (N) {
@@ -783,22 +48,8 @@ static int e_of(int N) {
     case 5: return Tr<5>::E; case 6: return Tr<6>::E; case 7: return Tr<7>::E; default: return Tr<8>::E;
   }
 }
-static std::vector<double> tables_of(const RefOps& R) {
-  switch (R.N) {
-    case 1: return Impl<1>::build_tables(R); case 2: return Impl<2>::build_tables(R);
-    case 3: return Impl<3>::build_tables(R); case 4: return Impl<4>::build_tables(R);
-    case 5: return Impl<5>::build_tables(R); case 6: return Impl<6>::build_tables(R);
-    case 7: return Impl<7>::build_tables(R); default: return Impl<8>::build_tables(R);
-  }
-}
-static std::vector<double> diagtab_of(const RefOps& R) {
-  switch (R.N) {
-    case 1: return Impl<1>::build_diagtab(R); case 2: return Impl<2>::build_diagtab(R);
-    case 3: return Impl<3>::build_diagtab(R); case 4: return Impl<4>::build_diagtab(R);
-    case 5: return Impl<5>::build_diagtab(R); case 6: return Impl<6>::build_diagtab(R);
-    case 7: return Impl<7>::build_diagtab(R); default: return Impl<8>::build_diagtab(R);
-  }
-}
+static std::vector<double> tables_of(const RefOps& R) { return impl_ops(R.N)->build_tables(R); }
+static std::vector<double> diagtab_of(const RefOps& R) { return impl_ops(R.N)->build_diagtab(R); }
 
 // largest ghost count per block that keeps k_sipdg<N> (lambda variant) within the SM's
 // opt-in shared memory at one CTA per SM
@@ -823,23 +74,19 @@ static int ghost_cap(int N, int device) {
   }
 }
 
-template <class Tp>
-static int upload(ipdg_ctx c, Tp** dst, const Tp* src, size_t n) {
-  if (*dst) cudaFree(*dst);
-  *dst = nullptr;
-  CUDA_TRY(c, cudaMalloc((void**)dst, std::max<size_t>(n, 1) * sizeof(Tp)));
-  if (n) CUDA_TRY(c, cudaMemcpy(*dst, src, n * sizeof(Tp), cudaMemcpyHostToDevice));
-  return IPDG_OK;
-}
+static void free_ws(ipdg_ctx c);
 
+// drops every mesh-sized buffer, including the PCG workspace binding (its layout depends on K + H)
 static void free_mesh(ipdg_ctx c) {
-  void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
-                  c->t_boff, c->t_goff, c->t_gid, c->t_nbr};
+  free_ws(c);
+  if (c->hostio) cudaFree(c->hostio);
+  c->hostio = nullptr;
+  c->hostio_n = 0;
+  void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->geo = nullptr; c->gG = nullptr; c->gF = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
   c->nbg = nullptr; c->W2 = nullptr;
-  c->t_boff = nullptr; c->t_goff = nullptr; c->t_gid = nullptr; c->t_nbr = nullptr; c->t_nblocks = 0;
   c->bcode = nullptr;
   c->vxy = nullptr;
   for (auto& g : c->gexec)
@@ -927,7 +174,7 @@ int ipdg_create(ipdg_ctx* out, int N, int device) {
     delete c;
     return rc;
   }
-  if ((rc = [&]() -> int { DISPATCH(N, upload_tpe_constants(c)); }())) {
+  if ((rc = impl_ops(N)->upload_constants(c))) {
     delete c;
     return rc;
   }
@@ -1116,7 +363,22 @@ static int build_block_lists(ipdg_ctx c, int64_t K, const std::vector<int>& boff
   return IPDG_OK;
 }
 
+// debug grid cap (ipdg_debug_grid_cap): clamp every persistent grid so that small test meshes run
+// several element blocks per CTA (the prefetch / ring paths of the pipelined kernels)
+static void apply_grid_cap(ipdg_ctx c) {
+  const int cap = c->grid_cap;
+  if (cap <= 0) return;
+  for (auto& m : c->grid)
+    for (int& g : m) g = std::min(g, cap);
+  for (auto& m : c->grid_pipe)
+    for (int& g : m) if (g > 0) g = std::min(g, cap);
+  for (auto& m : c->grid_flux)
+    for (int& g : m) g = std::min(g, cap);
+  c->grid_grad = std::min(c->grid_grad, cap);
+}
+
 static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
+  free_ws(c);  // the workspace layout depends on K + H
   const int64_t K = c->pend_K;
   const int E = c->E;
   std::vector<int>& etoe = c->pend_etoe;
@@ -1128,14 +390,6 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   std::vector<int>& gid = S.gid;
   std::vector<short4>& nbr = S.nbr;
   const int gmax = S.gmax;
-  if (c->N <= 4) {  // thread-per-element variant: its own blocks (E = 128, <= 64 ghosts)
-    Schedule T = build_schedule(K, 128, 64, etoe, etof, bc);
-    c->t_nblocks = (int)T.boff.size() - 1;
-    TRY(upload(c, &c->t_boff, T.boff.data(), T.boff.size()));
-    TRY(upload(c, &c->t_goff, T.goff.data(), T.goff.size()));
-    TRY(upload(c, &c->t_gid, T.gid.data(), T.gid.size()));
-    TRY(upload(c, &c->t_nbr, T.nbr.data(), T.nbr.size()));
-  }
   const int nb = (int)boff.size() - 1;
   if (E + gmax > 32000) FAIL(c, IPDG_EMESH, "element ordering too scattered (a block has %d ghosts)", gmax);
   c->K = K;
@@ -1181,7 +435,9 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   k_geofacs<<<(unsigned)((KH + 255) / 256), 256>>>(K, KH, c->geo, c->etoe, c->bcode, c->tau_c, c->gG, c->gF);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
-  DISPATCH(c->N, configure(c));
+  TRY(impl_ops(c->N)->configure(c));
+  apply_grid_cap(c);
+  return IPDG_OK;
 }
 
 int ipdg_upload_halo(ipdg_ctx c, int64_t H, const int32_t* ghost_etov, const int32_t* remote, const int8_t* remote_face,
@@ -1395,7 +651,7 @@ int ipdg_set_workspace(ipdg_ctx c, void* dev, int64_t bytes) {
   int64_t need = 0;
   TRY(ipdg_workspace_bytes(c, &need));
   if (bytes < need) FAIL(c, IPDG_EINVAL, "workspace too small: %lld < %lld", (long long)bytes, (long long)need);
-  if (c->ws == dev && !c->ws_owned) return IPDG_OK;
+  // always re-bind: the segment offsets depend on the current mesh (K + H)
   free_ws(c);
   c->ws = dev;
   c->ws_bytes = bytes;
@@ -1404,9 +660,10 @@ int ipdg_set_workspace(ipdg_ctx c, void* dev, int64_t bytes) {
 }
 
 static int ensure_ws(ipdg_ctx c) {
-  if (c->ws) return IPDG_OK;
   int64_t need = 0;
   TRY(ipdg_workspace_bytes(c, &need));
+  if (c->ws && c->ws_bytes >= need) return IPDG_OK;
+  free_ws(c);
   CUDA_TRY(c, cudaMalloc(&c->ws, need));
   c->ws_owned = true;
   c->ws_bytes = need;
@@ -1433,7 +690,7 @@ static int allreduce(ipdg_ctx c, double* buf, int n, cudaStream_t s) {
   return IPDG_OK;
 }
 
-static int vec_grid(ipdg_ctx c) { return std::min(c->sms * 8, 4096); }
+static int vec_grid(ipdg_ctx c) { return c->grid_cap > 0 ? c->grid_cap : std::min(c->sms * 8, 4096); }
 
 static int halo_for_p(ipdg_ctx c, cudaStream_t s) {
   if (c->H == 0 && c->S == 0) return IPDG_OK;
@@ -1458,12 +715,7 @@ static int pass_b(ipdg_ctx c, cudaStream_t s) {
 
 static int resolved_pass_a(ipdg_ctx c) {
   const bool lam = c->lambda != 0.0;
-  switch (c->N) {
-    case 1: return Impl<1>::resolve(c, 1, lam, c->x); case 2: return Impl<2>::resolve(c, 1, lam, c->x);
-    case 3: return Impl<3>::resolve(c, 1, lam, c->x); case 4: return Impl<4>::resolve(c, 1, lam, c->x);
-    case 5: return Impl<5>::resolve(c, 1, lam, c->x); case 6: return Impl<6>::resolve(c, 1, lam, c->x);
-    case 7: return Impl<7>::resolve(c, 1, lam, c->x); default: return Impl<8>::resolve(c, 1, lam, c->x);
-  }
+  return impl_ops(c->N)->resolve(c, 1, lam, c->x);
 }
 
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
@@ -1538,11 +790,7 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   // x is updated by pass A (deferred x += alpha_{k-1} p_{k-1}) -- measured faster on C2 than x += alpha_k p_k
   // in pass B (pass B 18 -> 29 us, pass A -3 us) -- unless k_pipe would lose a resident CTA per SM to the
   // x staging buffer (e.g. the lambda variant at N = 4), then pass B updates x.
-  c->xb = [&]() -> bool { switch (c->N) {
-      case 1: return Impl<1>::resolve(c, 1, lambda != 0.0, x) == 4; case 2: return Impl<2>::resolve(c, 1, lambda != 0.0, x) == 4;
-      case 3: return Impl<3>::resolve(c, 1, lambda != 0.0, x) == 4; case 4: return Impl<4>::resolve(c, 1, lambda != 0.0, x) == 4;
-      case 5: return Impl<5>::resolve(c, 1, lambda != 0.0, x) == 4; case 6: return Impl<6>::resolve(c, 1, lambda != 0.0, x) == 4;
-      case 7: return Impl<7>::resolve(c, 1, lambda != 0.0, x) == 4; default: return Impl<8>::resolve(c, 1, lambda != 0.0, x) == 4; } }()
+  c->xb = impl_ops(c->N)->resolve(c, 1, lambda != 0.0, x) == 4
            && c->pipe_xb[lambda != 0.0];
   PcgState h;
   std::memset(&h, 0, sizeof(h));
@@ -1692,19 +940,24 @@ int ipdg_pcg_solve_host(ipdg_ctx c, const double* b_host, double* x_host, double
   cudaStream_t s = (cudaStream_t)stream;
   TRY(ensure_ws(c));
   const int64_t n = c->K * c->ref.Np;
-  // b goes through the Ap slot of a separate buffer pair: allocate two vectors once
-  static thread_local double* bx = nullptr;
-  static thread_local int64_t bx_n = 0;
-  if (bx_n < n) {
-    if (bx) cudaFree(bx);
-    CUDA_TRY(c, cudaMalloc(&bx, 2 * n * sizeof(double)));
-    bx_n = n;
+  // per-context device staging of b and x on the context's device, each vector 256-byte aligned (the
+  // pipelined kernels move rows with bulk copies); allocated once per mesh, freed with it, so repeated
+  // calls reuse the same pointers and the captured iteration graphs
+  const int64_t seg = (n * 8 + 255) / 256 * 256 / 8;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->hostio_n < seg) {
+    if (c->hostio) cudaFree(c->hostio);
+    c->hostio = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->hostio, 2 * seg * sizeof(double)));
+    c->hostio_n = seg;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(bx, b_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  CUDA_TRY(c, cudaMemcpyAsync(bx + n, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  const int rc = ipdg_pcg_solve(c, bx, bx + n, lambda, precond, tol, maxit, stats, stream);
+  double* bd = c->hostio;
+  double* xd = c->hostio + c->hostio_n;
+  CUDA_TRY(c, cudaMemcpyAsync(bd, b_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(xd, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  const int rc = ipdg_pcg_solve(c, bd, xd, lambda, precond, tol, maxit, stats, stream);
   if (rc < 0) return rc;
-  CUDA_TRY(c, cudaMemcpyAsync(x_host, bx + n, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(x_host, xd, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
   return rc;
 }
@@ -1790,11 +1043,7 @@ int ipdg_get_connectivity(ipdg_ctx c, int32_t* etoe, int32_t* etof, int64_t cap)
 int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   if (!c || !out) return IPDG_EINVAL;
   // resolved pass-A kernel for lambda = 0 and its launch shape
-  const int kern = [&]() -> int { switch (c->N) {
-      case 1: return Impl<1>::resolve(c, 1, false, nullptr); case 2: return Impl<2>::resolve(c, 1, false, nullptr);
-      case 3: return Impl<3>::resolve(c, 1, false, nullptr); case 4: return Impl<4>::resolve(c, 1, false, nullptr);
-      case 5: return Impl<5>::resolve(c, 1, false, nullptr); case 6: return Impl<6>::resolve(c, 1, false, nullptr);
-      case 7: return Impl<7>::resolve(c, 1, false, nullptr); default: return Impl<8>::resolve(c, 1, false, nullptr); } }();
+  const int kern = [&]() -> int { return impl_ops(c->N)->resolve(c, 1, false, nullptr); }();
   const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : (int64_t)c->smem[1][0];
   const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : c->grid[1][0];
   const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0],
@@ -1838,8 +1087,23 @@ int ipdg_debug_split_pass_a(ipdg_ctx c, int on) {
   return IPDG_OK;
 }
 
+// debug (not in ipdg.h): cap every persistent grid at `cap` CTAs (0 = off) so that a small mesh takes
+// several element blocks per CTA; applies to the current mesh and every later upload.
+int ipdg_debug_grid_cap(ipdg_ctx c, int cap) {
+  if (!c || cap < 0) return IPDG_EINVAL;
+  c->grid_cap = cap;
+  if (c->K > 0) {
+    TRY(impl_ops(c->N)->configure(c));
+    apply_grid_cap(c);
+  }
+  for (auto& g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  c->gkey_x = nullptr;
+  return IPDG_OK;
+}
+
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 5 || ((variant == 3 || variant == 5) && c->N > 4)) return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 5 || variant == 3 || (variant == 5 && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

@@ -71,6 +71,9 @@ __host__ __device__ __forceinline__ constexpr int fmask_cf(int f, int k) {
 // (80 B each) are a 16-byte multiple for a bulk copy
 constexpr int kGF = 10;
 
+// k_gather: threads per CTA (one element per thread)
+constexpr int kGatherThreads = 128;
+
 // Kernel parameters (plain pointers; all device memory).
 struct AxArgs {
   int64_t K;             // local elements

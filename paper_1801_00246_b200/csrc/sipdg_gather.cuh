@@ -6,20 +6,20 @@
 // "one thread to one element" mapping): its own row and geometry records, and per interior face the
 // neighbour's row and chain-rule record (L1/L2 hits: the neighbour is a nearby element in Morton order),
 // from which it recomputes the neighbour's normal-derivative trace on the shared face only.
-// The operators are compile-time indices into __constant__ memory (c_tpe, sipdg_tpe.cuh).
+// The operators are compile-time indices into __constant__ memory (c_tpe, cops.cuh).
 //   volume:  Au = Sr^T w_r + Ss^T w_s,  w = J G (Dr u, Ds u)          (Alg. AxG)
 //   faces:   + (LIFT_f^T Sr)^T c_r delta + (LIFT_f^T Ss)^T c_s delta - E_f (sJ g)  (Alg. AxKernel)
 //   PCG pass A: p_k = z + beta p_{k-1} formed for the own and the neighbour rows (one FMA, identical
 //   everywhere), p_k and the deferred x update written for the own row, p.Ap reduced.
 #pragma once
 #include "sipdg_split.cuh"
-#include "sipdg_tpe.cuh"
+#include "cops.cuh"
 
 namespace ipdg {
 
 // threads per CTA of k_gather: small CTAs so register-heavy instantiations still fill an SM in steps
 // of 4 warps
-constexpr int kGatherThreads = 128;
+
 
 // neighbour element `n` seen through its face FP: its values and traces sJ n.grad u (its own outward
 // normal) at the face nodes, in its own face order

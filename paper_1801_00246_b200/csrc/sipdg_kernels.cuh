@@ -64,7 +64,7 @@ enum { MODE_AX = 0, MODE_PCG_A = 1 };
 // Optional phase timing (compile with -DIPDG_PHASE_TIMING; tools/phase_timing.py): warp 0 of every
 // CTA accumulates clock64() deltas per phase into ipdg_phase_cycles[8].
 #ifdef IPDG_PHASE_TIMING
-__device__ unsigned long long ipdg_phase_cycles[8];
+static __device__ unsigned long long ipdg_phase_cycles[8];
 #define PHASE_MARK(id)                                                   \
   do {                                                                   \
     if (threadIdx.x == 0) {                                              \
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_sipdg(AxArgs a, 
 
 // ---- PCG pass B: r -= alpha A p; z = D^{-1} r; partial (r.z, r.r)
 // With x != null (k_pipe protocol) it also applies x += alpha_k p_k (p_k from pass A of this iteration)
-__global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r, const double* __restrict__ Ap,
+static __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r, const double* __restrict__ Ap,
                                                const double* __restrict__ dinv, double* __restrict__ z, PcgState* st,
                                                double* partials, unsigned int* counter, double* __restrict__ x,
                                                const double* p_even, const double* p_odd) {
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restrict__ r
 }
 
 // ---- PCG start: r = b - A x0, partial (r.z, r.r, b.b)
-__global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
+static __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
                                                   double* __restrict__ r, const double* __restrict__ dinv,
                                                   double* __restrict__ z, PcgState* st, double* partials,
                                                   unsigned int* counter) {
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const double* __res
 }
 
 // ---- finalize: apply the pending x += alpha_k p_k when the loop ended without a stop decision
-__global__ void __launch_bounds__(256) k_pcg_final_x(int64_t n, double* __restrict__ x, const double* p_even,
+static __global__ void __launch_bounds__(256) k_pcg_final_x(int64_t n, double* __restrict__ x, const double* p_even,
                                                      const double* p_odd, const PcgState* st) {
   if (st->stop_iter >= 0) return;
   const long long k = st->it;
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(256) k_pcg_final_x(int64_t n, double* __restri
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] += alpha * p[i];
 }
-__global__ void k_pcg_final_state(PcgState* st) {
+static __global__ void k_pcg_final_state(PcgState* st) {
   if (st->stop_iter >= 0) return;
   const long long k = st->it;
   st->stop_iter = k;
@@ -739,7 +739,7 @@ __global__ void k_mass(int64_t K, const double4* __restrict__ geo, const double*
   Mu[idx] = J * s;
 }
 
-__global__ void k_nodes(int64_t K, int NP, const double* __restrict__ vxy, const double* __restrict__ rs,
+static __global__ void k_nodes(int64_t K, int NP, const double* __restrict__ vxy, const double* __restrict__ rs,
                         double* __restrict__ x, double* __restrict__ y) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= K * NP) return;
@@ -752,7 +752,7 @@ __global__ void k_nodes(int64_t K, int NP, const double* __restrict__ vxy, const
 }
 
 // ---- geometric factors from vertex coordinates (Eq. operators2): r_x = y_s/J, ... ; J <= 0 flagged
-__global__ void k_geometry(int64_t K, const double* __restrict__ vxy, double4* __restrict__ geo,
+static __global__ void k_geometry(int64_t K, const double* __restrict__ vxy, double4* __restrict__ geo,
                            unsigned long long* bad) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= K) return;

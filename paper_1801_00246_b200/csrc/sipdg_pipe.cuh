@@ -106,7 +106,7 @@ __host__ __device__ inline int node_trace_cols(int i, int JUNK) {
 //   gG[e] = (J G_rr, J G_rs, J G_ss, J), G_rr = r_x^2 + r_y^2, G_rs = r_x s_x + r_y s_y, G_ss = s_x^2 + s_y^2
 //   gF[e][3f..3f+2] = (1/2 sJ n.grad r, 1/2 sJ n.grad s, sJ tau_f) with sJ n = J g_f,
 //   g_f = -grad s, grad r + grad s, -grad r, and sJ tau_f = tau_c sJ^2 max(1/J, 1/J+) (1/h = sJ/J)
-__global__ void k_geofacs(int64_t K, int64_t KH, const double4* __restrict__ geo, const int* __restrict__ etoe,
+static __global__ void k_geofacs(int64_t K, int64_t KH, const double4* __restrict__ geo, const int* __restrict__ etoe,
                           const int8_t* __restrict__ bcode, double tau_c, double4* __restrict__ gG,
                           double* __restrict__ gF) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -143,3 +143,38 @@ def test_exact_lagrange_basis_matches_float(N):
         vals = [float(sum(c * Fraction(r) ** a * Fraction(s) ** b for (a, b), c in p.items()))
                 for r, s in zip(re.r.tolist(), re.s.tolist())]
         assert np.allclose(vals, np.eye(re.Np)[i], atol=1e-14)
+
+
+def _lebesgue(ref, m=300):
+    """max over a uniform grid of the triangle of sum_i |l_i| (the Lebesgue function)."""
+    i, j = np.meshgrid(np.arange(m + 1), np.arange(m + 1), indexing="ij")
+    keep = (i + j) <= m
+    r = -1.0 + 2.0 * i[keep] / m
+    s = -1.0 + 2.0 * j[keep] / m
+    return np.abs(ref.eval_basis(r, s)).sum(axis=1).max()
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_warp_blend_lebesgue_constants(k):
+    """The interior Warp & Blend nodes for N >= 3 (alpha_opt table, P:56 via Warburton 2006) are pinned by
+    their published Lebesgue constants (Hesthaven & Warburton 2008, Table 6.1; tests/golden): a wrong
+    blend, warp or alpha entry moves the constant in the second decimal for N >= 6."""
+    g = GOLD["lebesgue_warp_blend"]
+    N = g["N"][k]
+    assert abs(_lebesgue(RefElem(N), m=150 + 50 * N) - g["alpha_opt"][k]) <= 0.006, N
+
+
+def test_warp_blend_lebesgue_alpha_zero():
+    """The same construction with the blending switched off (alpha = 0) reproduces the table's
+    alpha = 0 column, and alpha_opt improves on it -- an independent check of the warp itself."""
+    import oracle.refelem as R
+    g = GOLD["lebesgue_warp_blend"]["alpha_zero"]
+    for N, val in zip(g["N"], g["value"]):
+        saved = R.ALPHA_OPT[N - 1]
+        try:
+            R.ALPHA_OPT[N - 1] = 0.0
+            lz = _lebesgue(RefElem(N))
+        finally:
+            R.ALPHA_OPT[N - 1] = saved
+        assert abs(lz - val) <= 0.006, N
+        assert _lebesgue(RefElem(N)) < lz - 0.1
