@@ -1,0 +1,38 @@
+"""Test helper: the oracle PCG's own iteration-count spread under reorderings of the unknowns (DESIGN.md
+reading R15).  Calls only oracle/ code."""
+import numpy as np
+
+from oracle import solvers
+
+
+def oracle_iteration_spread(A, b, tol, maxit, precond, lam, ref, m, seeds=(1, 2, 3)):
+    """Oracle PCG iteration counts on the system as given and under random symmetric permutations of the
+    unknowns (P A P^T, P b): the same mathematics with every sum in a different order.  Returns (x of the
+    unpermuted solve, its stats, the sorted list of counts)."""
+    n = b.size
+    dinv = 1.0 / A.diagonal() if precond == 1 else None
+    Pb = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam) if precond == 2 else None
+    x, st = solvers.pcg(lambda v: A @ v, b, tol, maxit, dinv=dinv, apply_P=Pb)
+    counts = [st["iterations"]]
+    for seed in seeds:
+        perm = np.random.default_rng(seed).permutation(n)
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(n)
+        Ap = A[perm][:, perm].tocsr()
+        if precond == 2:
+            def P(r, perm=perm, inv=inv):
+                return Pb(r[inv])[perm]
+        else:
+            P = None
+        _, sp = solvers.pcg(lambda v: Ap @ v, b[perm], tol, maxit, dinv=None if dinv is None else dinv[perm], apply_P=P)
+        counts.append(sp["iterations"])
+    return x, st, sorted(counts)
+
+
+def check_iterations(gpu_it, it_o, counts):
+    """North star: +-1 of the oracle; where the oracle itself moves under a reordering of the unknowns, the
+    GPU count must lie within the oracle's spread +-1 (R15)."""
+    lo, hi = min(counts) - 1, max(counts) + 1
+    assert lo <= gpu_it <= hi, (gpu_it, it_o, counts)
+    if counts[0] == counts[-1]:
+        assert abs(gpu_it - it_o) <= 1, (gpu_it, it_o, counts)

@@ -10,6 +10,7 @@ from oracle import solvers  # noqa: E402
 from oracle.assemble import assemble  # noqa: E402
 from oracle.refelem import RefElem  # noqa: E402
 from paper_1801_00246_b200 import Ipdg, IpdgError, meshgen  # noqa: E402
+from pcg_spread import check_iterations, oracle_iteration_spread  # noqa: E402
 
 
 def gpu(x):
@@ -23,16 +24,13 @@ def check_solve(m, N, precond, tol, lam=0.0, maxit=20000, f=meshgen.sin_sin_forc
     op = Ipdg(N, m)
     op.set_variant(variant)
     x, st = op.pcg_solve(gpu(b), lam=lam, precond=precond, tol=tol, maxit=maxit)
-    dinv = 1.0 / A.diagonal() if precond == 1 else None
-    P = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam) if precond == 2 else None
-    xo, sto = solvers.pcg(lambda v: A @ v, b.ravel(), tol, maxit, dinv=dinv, apply_P=P)
+    xo, sto, counts = oracle_iteration_spread(A, b.ravel(), tol, maxit, precond, lam, ref, m)
     assert st["status"] == sto["status"] == 0
-    # +-1 iteration (north star); on solves of several hundred iterations the rounding-order
-    # differences (FMA contraction, DMMA accumulation, reduction trees) may move the count by up to
-    # 0.5 % (reading R15) -- the solution is then held to the oracle's residual below
-    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"])), (st, sto["iterations"])
+    # +-1 iteration (north star), widened only by the oracle's own spread under reorderings (R15)
+    check_iterations(st["iterations"], sto["iterations"], counts)
+    true_o = np.linalg.norm(b.ravel() - A @ xo) / np.linalg.norm(b)
     r = b.ravel() - A @ x.cpu().numpy().ravel()
-    assert np.linalg.norm(r) <= tol * np.linalg.norm(b) * (1 + 1e-6) * 1.01
+    assert np.linalg.norm(r) <= max(tol, true_o) * np.linalg.norm(b) * (1 + 1e-6)
     assert abs(st["bnorm"] - np.linalg.norm(b)) <= 1e-13 * np.linalg.norm(b)
     return op, st, sto
 
@@ -54,9 +52,9 @@ def test_jacobi_mixed_boundaries(N):
 def test_jacobi_nearly_neumann_long_solve(N):
     """Dirichlet only on the edge x = 1 (cylinder-like pressure problem): ~1700 iterations.
 
-    Over that many iterations the FMA contraction and the summation order of the GPU
-    reductions perturb CG's short recurrences at the rounding level, so the iteration count
-    may move by a few (reading R15); the solution is held to the oracle's residual."""
+    Over that many iterations the summation order perturbs CG's short recurrences at the rounding
+    level: the oracle itself moves by several iterations when the unknowns are reordered, and the GPU
+    count is held to that measured spread +-1 (reading R15)."""
     m = meshgen.square(10, jitter=0.2, diag="random", order="morton", seed=6,
                        tag=lambda x, y: np.where(x > 0.95, 1, 2).astype(np.int8))
     ref = RefElem(N)
@@ -65,14 +63,15 @@ def test_jacobi_nearly_neumann_long_solve(N):
     b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, f)
     op = Ipdg(N, m)
     x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-8, maxit=20000)
-    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-8, 20000, dinv=1.0 / A.diagonal())
+    xo, sto, counts = oracle_iteration_spread(A, b.ravel(), 1e-8, 20000, 1, 0.0, ref, m)
     assert st["status"] == sto["status"] == 0
-    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    check_iterations(st["iterations"], sto["iterations"], counts)
+    true_o = np.linalg.norm(b.ravel() - A @ xo) / np.linalg.norm(b)
     r = b.ravel() - A @ x.cpu().numpy().ravel()
-    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b) * 1.05
+    assert np.linalg.norm(r) <= max(1e-8, true_o) * np.linalg.norm(b) * (1 + 1e-6)
 
 
-@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 3), (2, 3), (3, 3), (4, 3), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5)])
+@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5)])
 def test_pcg_other_kernel_variant(N, variant):
     m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=13)
     check_solve(m, N, 1, 1e-9, variant=variant)
@@ -158,18 +157,19 @@ def test_split_pass_a_two_launch_reduction(N):
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     assert fn(op.ctx, 1) == 0
     x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-9, maxit=5000)
-    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-9, 5000, dinv=1.0 / A.diagonal())
+    xo, sto, counts = oracle_iteration_spread(A, b.ravel(), 1e-9, 5000, 1, 0.0, ref, m)
     assert st["status"] == sto["status"] == 0
-    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    check_iterations(st["iterations"], sto["iterations"], counts)
+    true_o = np.linalg.norm(b.ravel() - A @ xo) / np.linalg.norm(b)
     r = b.ravel() - A @ x.cpu().numpy().ravel()
-    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b) * 1.01
+    assert np.linalg.norm(r) <= max(1e-9, true_o) * np.linalg.norm(b) * (1 + 1e-6)
 
 
 def test_c4_recipe_small_cylinder():
     """BASELINE config C4 recipe at a small size (the channel with the square cylinder, graded, outflow
     Dirichlet, inflow / walls / cylinder Neumann, f = exp(-((x-2)^2 + y^2)/4)): Ax parity at N = 6 and
-    the Jacobi-PCG solve at N = 3 against the oracle (~4000 iterations: count within DESIGN.md R15,
-    solution held to the oracle's residual)."""
+    the Jacobi-PCG solve at N = 3 against the oracle (~4000 iterations: count within the oracle's own
+    reordering spread +-1, R15; solution held to the oracle's residual)."""
     m = meshgen.cylinder(h0=0.1, ratio=1.3)
     ref6 = RefElem(6)
     A6 = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref6)
@@ -184,8 +184,9 @@ def test_c4_recipe_small_cylinder():
     b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref3, f)
     op = Ipdg(3, m)
     x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-8, maxit=20000)
-    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-8, 20000, dinv=1.0 / A.diagonal())
+    xo, sto, counts = oracle_iteration_spread(A, b.ravel(), 1e-8, 20000, 1, 0.0, ref3, m)
     assert st["status"] == sto["status"] == 0
-    assert abs(st["iterations"] - sto["iterations"]) <= max(1, int(0.005 * sto["iterations"]))
+    check_iterations(st["iterations"], sto["iterations"], counts)
+    true_o = np.linalg.norm(b.ravel() - A @ xo) / np.linalg.norm(b)
     r = b.ravel() - A @ x.cpu().numpy().ravel()
-    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b) * 1.05
+    assert np.linalg.norm(r) <= max(1e-8, true_o) * np.linalg.norm(b) * (1 + 1e-6)

@@ -99,7 +99,7 @@ __global__ void k_dmma884(double* out, double a, double b) {
 __global__ void k_dmma1684(double* out, double a, double b) {
   double c[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) c[i][j] = threadIdx.x + j;
+  for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) c[i][j] = threadIdx.x + j + 7 * i;  // distinct chains (identical ones are merged by ptxas)
   for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) dmma1684(c[i], a, b, a);
@@ -116,7 +116,7 @@ __global__ void k_dmma16816(double* out, double a, double b) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) bv[i] = b + i;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) c[i][j] = threadIdx.x + j;
+  for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) c[i][j] = threadIdx.x + j + 7 * i;  // distinct chains (identical ones are merged by ptxas)
   for (int it = 0; it < ITERS / 16; ++it) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) dmma16816(c[i], av, bv);

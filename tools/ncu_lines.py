@@ -1,40 +1,22 @@
-"""Aggregate an ncu source page (cuda,sass csv) per CUDA source line: stall samples + instructions."""
-import csv
-import sys
-from collections import defaultdict
-
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-hdr = None
-agg = defaultdict(lambda: [0.0, 0.0, ""])
-stall_cols = []
-per_stall = defaultdict(float)
+"""Per-source-line instructions executed per unit and warp-stall samples (top reasons) of an ncu source page.
+usage: ncu -i rep --page source --csv --print-source cuda,sass [--launch-skip i --launch-count 1] > src.csv
+       python tools/ncu_lines.py src.csv <units, e.g. elements>"""
+import csv,sys
+rows=list(csv.reader(open(sys.argv[1])))
+units=float(sys.argv[2])
+fname="";hdr=None;out=[]
 for r in rows:
-    if len(r) > 5 and r[0] == "Line No":
-        hdr = r
-        idx = {h: j for j, h in enumerate(hdr)}
-        stall_cols = [(h, j) for j, h in enumerate(hdr) if h.startswith("stall_")]
-        continue
-    if hdr is None or len(r) != len(hdr):
-        continue
-    if r[0] not in ("-", ""):
-        ln = r[0]
-        s = float(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
-        ie = float(r[idx["Instructions Executed"]] or 0)
-        agg[ln][0] += s
-        agg[ln][1] += ie
-        agg[ln][2] = r[1][:100]
-        for h, j in stall_cols:
-            try:
-                per_stall[h] += float(r[j] or 0)
-            except ValueError:
-                pass
-tot = sum(v[0] for v in agg.values()) or 1
-tot_i = sum(v[1] for v in agg.values()) or 1
-print("total samples %.0f, instructions %.0f" % (tot, tot_i))
-for ln, (s, ie, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print("%5.1f%% samp %5.1f%% inst  L%-4s %s" % (100 * s / tot, 100 * ie / tot_i, ln, src))
-print("stall reasons:")
-st = sum(per_stall.values()) or 1
-for h, v in sorted(per_stall.items(), key=lambda kv: -kv[1])[:12]:
-    print("  %-28s %5.1f%%" % (h, 100 * v / st))
+    if len(r)==2 and r[0]=="File Path": fname=r[1].split('/')[-1]; continue
+    if r and r[0]=="Line No": hdr=r; continue
+    if hdr is None or len(r)<10 or r[0]=="" : continue
+    d=dict(zip(hdr,r))
+    try: n=int(d["Instructions Executed"]); s=int(d["Warp Stall Sampling (All Samples)"])
+    except: continue
+    st={k[6:]:int(v) for k,v in d.items() if k.startswith('stall_') and '(' not in k and v.isdigit() and int(v)>0}
+    top=sorted(st.items(),key=lambda x:-x[1])[:3]
+    out.append((fname,int(r[0]),n/units,s,top,r[1].strip()[:70]))
+tot=sum(o[2] for o in out); ts=sum(o[3] for o in out)
+print("instr/unit %.1f samples %d"%(tot,ts))
+for o in out:
+    if o[2]>=0.8 or o[3]>=ts*0.008:
+        print("%-16s %4d %6.2f %5.1f%% %-40s %s"%(o[0],o[1],o[2],100*o[3]/ts,",".join("%s:%d"%t for t in o[4]),o[5]))

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--N", type=int, default=4)
     ap.add_argument("--K", type=int, default=199712)
+    ap.add_argument("--iteration", type=int, default=None, help="PCG iteration of the captured pass-A launch")
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -78,7 +79,8 @@ def main():
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     if pa:
         summ["pass_a"] = {"N": a.N, "K": a.K, "kernel": kname(pa[0]), "dram_bytes_per_launch": pa[0].get("dram_bytes"),
-                          "duration_us_under_ncu": pa[0].get("duration_us"), "source": os.path.basename(a.rep)}
+                          "duration_us_under_ncu": pa[0].get("duration_us"), "source": os.path.basename(a.rep),
+                          "pcg_iteration": a.iteration}
     ax = [d for d in out if ("<%d, 0" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe")]
     if ax:
         summ["ax"] = {"N": a.N, "K": a.K, "kernel": kname(ax[0]), "dram_bytes_per_launch": ax[0].get("dram_bytes"),
