@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libipdg.so")
+LIB_PATH = os.environ.get("IPDG_LIB") or os.path.join(HERE, "libipdg.so")  # IPDG_LIB: A/B timing of library builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ipdg.h")
 
 IPDG_OK = 0

@@ -539,12 +539,13 @@ __global__ void __launch_bounds__(Tr<N>::W * 32, Tr<N>::MINB) k_pipe(AxArgs a, i
         const double* b0 = tabM + (KCW + q) * NT * 32 + lane;
         const double* b1 = tabM + (KCW + T::NQ + q) * NT * 32 + lane;
         const double* b2 = tabM + (KCW + 2 * T::NQ + q) * NT * 32 + lane;
+        // chains interleaved: consecutive DMMAs go to different accumulators (26.6-cycle DMMA latency)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          dmma(C[j][0], C[j][1], far, b0[j * 32]);
-          dmma(C[j][0], C[j][1], fas, b1[j * 32]);
-          dmma(C[j][0], C[j][1], fag, b2[j * 32]);
-        }
+        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], far, b0[j * 32]);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], fas, b1[j * 32]);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(C[j][0], C[j][1], fag, b2[j * 32]);
       }
       if (LAM) {
         const double lj = a.lambda * gGs[ec * 4 + 3];

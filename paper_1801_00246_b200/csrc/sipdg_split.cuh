@@ -113,29 +113,66 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
   for (int i = lane; i < 8 * SU; i += 32) st8[i] = 0.0;
   __syncthreads();
   // rows [ebeg, eend): all K + H rows, or the own rows and then the halo rows (the latter after the
-  // halo exchange, which the own rows overlap)
+  // halo exchange, which the own rows overlap).  Software pipeline: the operand rows (PCG: z, p_{k-1}, x)
+  // and the geometry record of tile t + stride are loaded into registers while tile t computes.
+  constexpr int NPF = (8 * NP + 31) / 32;  // row values per lane for one 8-element tile
+  // prefetching costs registers (occupancy): measured faster for PCG pass A at N = 6, 8 and for Ax at N = 8,
+  // slower for Ax at N = 6 (C3: 636 -> 661 us), so Ax at N <= 6 loads each tile when it starts it
+  constexpr bool PF = (MODE == MODE_PCG_A) || N >= 7;
   const int64_t ntiles = (a.eend - a.ebeg + 7) / 8;
-  for (int64_t t = (int64_t)blockIdx.x * W + warp; t < ntiles; t += (int64_t)gridDim.x * W) {
+  const int64_t tstride = (int64_t)gridDim.x * W;
+  double pv[NPF], pp[NPF], px[NPF];
+  double4 pg = make_double4(0, 0, 0, 0);
+  auto fetch = [&](int64_t t) {
     const int64_t e0 = a.ebeg + 8 * t;
     const int nrow = (int)min((int64_t)8, a.eend - e0);
-    __syncwarp();
-    for (int q = lane; q < nrow * NP; q += 32) {  // operand rows of the tile (contiguous for own rows)
-      const int el = q / NP, i = q - el * NP;
-      const int64_t e = e0 + el;
-      double v;
-      if (e >= K) {
-        v = a.halo[(e - K) * NP + i];
-      } else if (MODE == MODE_AX) {
-        v = __ldg(a.u + e * NP + i);
-      } else {
-        const int64_t g = e * NP + i;
-        const double po = d.first ? 0.0 : pold[g];
-        v = __ldg(a.z + g) + d.beta * po;
-        pnew[g] = v;
-        if (d.do_xupd) a.x[g] += d.alpha_prev * po;
+#pragma unroll
+    for (int r = 0; r < NPF; ++r) {
+      const int q = lane + 32 * r;
+      pv[r] = pp[r] = px[r] = 0.0;
+      if (q < nrow * NP) {
+        const int el = q / NP, i = q - el * NP;
+        const int64_t e = e0 + el;
+        if (e >= K) {
+          pv[r] = a.halo[(e - K) * NP + i];
+        } else if (MODE == MODE_AX) {
+          pv[r] = __ldg(a.u + e * NP + i);
+        } else {
+          const int64_t g = e * NP + i;
+          pv[r] = __ldg(a.z + g);
+          if (!d.first) pp[r] = pold[g];
+          if (d.do_xupd) px[r] = a.x[g];
+        }
       }
-      st8[el * SU + i] = v;
     }
+    const int64_t e = e0 + (lane >> 2);
+    if (e < a.eend) pg = a.gG[e];
+  };
+  int64_t t = (int64_t)blockIdx.x * W + warp;
+  if (PF && t < ntiles) fetch(t);
+  for (; t < ntiles; t += tstride) {
+    const int64_t e0 = a.ebeg + 8 * t;
+    const int nrow = (int)min((int64_t)8, a.eend - e0);
+    if (!PF) fetch(t);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NPF; ++r) {  // operand rows of the tile (contiguous for own rows)
+      const int q = lane + 32 * r;
+      if (q < nrow * NP) {
+        const int el = q / NP, i = q - el * NP;
+        const int64_t e = e0 + el;
+        double v = pv[r];
+        if (MODE == MODE_PCG_A && e < K) {
+          const int64_t g = e * NP + i;
+          v = pv[r] + d.beta * pp[r];
+          pnew[g] = v;
+          if (d.do_xupd) a.x[g] = px[r] + d.alpha_prev * pp[r];
+        }
+        st8[el * SU + i] = v;
+      }
+    }
+    const double4 gr = pg;  // J G^T G from the setup records (k_geofacs)
+    if (PF && t + tstride < ntiles) fetch(t + tstride);
     __syncwarp();
     double acc[2 * NT][2];
 #pragma unroll
@@ -150,7 +187,6 @@ __global__ void __launch_bounds__(TrS<N>::W * 32) k_grad(SplitArgs a) {
     }
     const int64_t e = e0 + (lane >> 2);
     if (e < a.eend) {
-      const double4 gr = a.gG[e];  // J G^T G from the setup records (k_geofacs)
       const double Grr = gr.x, Grs = gr.y, Gss = gr.z;
       double* wrow = a.W2 + e * 2 * NP;
 #pragma unroll
