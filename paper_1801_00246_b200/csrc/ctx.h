@@ -50,12 +50,7 @@ struct ipdg_ctx_s {
   // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit
   size_t smem_pipe[2][2] = {{0, 0}, {0, 0}};
   int grid_pipe[2][2] = {{0, 0}, {0, 0}};
-  bool pipe_xb[2] = {false, false};
-  // warp-specialised variant (k_ws, N <= 5); grid 0 = does not fit
-  size_t smem_ws[2][2] = {{0, 0}, {0, 0}};
-  int grid_ws[2][2] = {{0, 0}, {0, 0}};
-  int occ_ws[2][2] = {{0, 0}, {0, 0}};
-  double* zero_row = nullptr;  // 64 zeros (k_ws: p_{k-1} of halo ghosts)  // [lam]: k_pipe's pass A leaves x to pass B (no room for x staging)
+  bool pipe_xb[2] = {false, false};  // [lam]: k_pipe's pass A leaves x to pass B (no room for x staging)
   size_t smem_grad = 0, smem_flux[2] = {0, 0};
   int grid_grad = 0, grid_flux[2][2] = {{0, 0}, {0, 0}};
   size_t smem[2][2] = {{0, 0}, {0, 0}};  // [mode][lam]

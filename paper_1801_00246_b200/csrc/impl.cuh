@@ -7,7 +7,6 @@
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
 #include "sipdg_pipe.cuh"
-#include "sipdg_ws.cuh"
 #include "pcg_blockjacobi.cuh"
 #include "cops.cuh"
 #include "sipdg_gather.cuh"
@@ -198,31 +197,7 @@ struct Impl {
         c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
       }
     }
-    TRY(configure_pipe(c, optin));
-    return configure_ws(c, optin);
-  }
-
-  // ---- warp-specialised pipelined variant (k_ws, N <= 5): producer warp + 4 compute warps
-  static int configure_ws(ipdg_ctx c, int optin) {
-    for (int lam = 0; lam < 2; ++lam)
-      for (int mode = 0; mode < 2; ++mode) {
-        c->grid_ws[mode][lam] = 0;
-        if constexpr (N <= 5) {
-          const void* fn = (mode == 0) ? (lam ? (const void*)k_ws<N, MODE_AX, true> : (const void*)k_ws<N, MODE_AX, false>)
-                                       : (lam ? (const void*)k_ws<N, MODE_PCG_A, true> : (const void*)k_ws<N, MODE_PCG_A, false>);
-          const WsLayout L = WsLayout::make<N>(c->gmax, lam != 0, mode == 1);
-          const size_t bytes = (size_t)L.total() * sizeof(double);
-          if ((int)bytes > optin - 1024) continue;
-          CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-          int occ = 0;
-          CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TrW<N>::NTHR, bytes));
-          if (occ < 1) continue;
-          c->smem_ws[mode][lam] = bytes;
-          c->occ_ws[mode][lam] = occ;
-          c->grid_ws[mode][lam] = (int)std::min<int64_t>(c->nblocks, (int64_t)occ * c->sms);
-        }
-      }
-    return IPDG_OK;
+    return configure_pipe(c, optin);
   }
 
   // ---- pipelined fused variant: needs room for the staging area next to the working rows
@@ -297,7 +272,6 @@ struct Impl {
     if (k == 0) k = (N >= 6) ? 2 : (N <= (mode == 0 ? 3 : 1) ? 5 : 4);
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
-    if (k == 6 && !(N <= 5 && c->grid_ws[mode][lam] > 0 && (mode == 1 || aligned16(v)))) k = 4;
     if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
     return k;
   }
@@ -427,7 +401,6 @@ struct Impl {
     a.nbg = c->nbg;
     a.tau_c = c->tau_c;
     a.halo_p = c->halobuf;
-    a.zero_row = c->zero_row;
     return a;
   }
 
@@ -440,16 +413,6 @@ struct Impl {
     a.Au = Au;
     a.lambda = lambda;
     if (k == 5) return launch_gather<MODE_AX>(c, a, lam, s);
-    if (k == 6) {
-      if constexpr (N <= 5) {
-        const int g = c->grid_ws[0][lam];
-        if (lam) k_ws<N, MODE_AX, true><<<g, TrW<N>::NTHR, c->smem_ws[0][1], s>>>(a, c->gmax);
-        else k_ws<N, MODE_AX, false><<<g, TrW<N>::NTHR, c->smem_ws[0][0], s>>>(a, c->gmax);
-        c->launches++;
-        CUDA_TRY(c, cudaGetLastError());
-        return IPDG_OK;
-      }
-    }
     if (k == 4) {
       const int gp = c->grid_pipe[0][lam];
       if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
@@ -484,30 +447,6 @@ struct Impl {
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
     if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
-    if (k == 6) {
-      if constexpr (N <= 5) {
-        const int gw = c->grid_ws[1][lam];
-        a.defer_x = 1;
-        auto launch = [&](int part, const int* list, int n) -> int {
-          a.blist = list;
-          a.nlist = n;
-          a.red_part = part;
-          const int cap = (part == 1 && c->halo_ev_pending) ? std::max(1, gw - kCommSlots) : gw;
-          const int g = list ? std::max(1, std::min(cap, n)) : gw;
-          if (lam) k_ws<N, MODE_PCG_A, true><<<g, TrW<N>::NTHR, c->smem_ws[1][1], s>>>(a, c->gmax);
-          else k_ws<N, MODE_PCG_A, false><<<g, TrW<N>::NTHR, c->smem_ws[1][0], s>>>(a, c->gmax);
-          c->launches++;
-          CUDA_TRY(c, cudaGetLastError());
-          return IPDG_OK;
-        };
-        if (c->split_a) {
-          TRY(launch(1, c->blist, c->nb_split[0]));
-          if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
-          return launch(2, c->blist + c->nb_split[0], c->nb_split[1]);
-        }
-        return launch(0, nullptr, 0);
-      }
-    }
     if (k == 4) {
       const int gp = c->grid_pipe[1][lam];
       auto launch = [&](int part, const int* list, int n) -> int {

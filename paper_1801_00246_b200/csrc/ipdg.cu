@@ -178,10 +178,6 @@ int ipdg_create(ipdg_ctx* out, int N, int device) {
     delete c;
     return rc;
   }
-  if (cudaMalloc(&c->zero_row, 64 * sizeof(double)) != cudaSuccess || cudaMemset(c->zero_row, 0, 64 * sizeof(double)) != cudaSuccess) {
-    delete c;
-    return IPDG_ECUDA;
-  }
   if (cudaMalloc(&c->st, sizeof(PcgState)) != cudaSuccess || cudaMallocHost(&c->st_host, sizeof(PcgState)) != cudaSuccess ||
       cudaMalloc(&c->counter, sizeof(unsigned int)) != cudaSuccess || cudaMemset(c->counter, 0, sizeof(unsigned int)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -200,7 +196,7 @@ int ipdg_destroy(ipdg_ctx c) {
   cudaSetDevice(c->device);
   free_mesh(c);
   free_ws(c);
-  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->Minv, c->dgops, c->st, c->counter, c->partials, c->zero_row};
+  void* ptrs[] = {c->tables, c->diagtab, c->rs, c->Mref, c->Minv, c->dgops, c->st, c->counter, c->partials};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st_host) cudaFreeHost(c->st_host);
@@ -378,8 +374,6 @@ static void apply_grid_cap(ipdg_ctx c) {
     for (int& g : m) if (g > 0) g = std::min(g, cap);
   for (auto& m : c->grid_flux)
     for (int& g : m) g = std::min(g, cap);
-  for (auto& m : c->grid_ws)
-    for (int& g : m) if (g > 0) g = std::min(g, cap);
   c->grid_grad = std::min(c->grid_grad, cap);
 }
 
@@ -726,7 +720,7 @@ static int resolved_pass_a(ipdg_ctx c) {
 
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
   const int kern = resolved_pass_a(c);
-  if (c->split_a && (kern == 4 || kern == 6 || (kern == 2 && c->H > 0))) {
+  if (c->split_a && (kern == 4 || (kern == 2 && c->H > 0))) {
     // halo exchange of p_k on the comm stream, overlapping the interior blocks of pass A
     c->halo_ev_pending = false;
     if ((c->H > 0 || c->S > 0) && !c->halo_external) {
@@ -1050,8 +1044,8 @@ int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   if (!c || !out) return IPDG_EINVAL;
   // resolved pass-A kernel for lambda = 0 and its launch shape
   const int kern = [&]() -> int { return impl_ops(c->N)->resolve(c, 1, false, nullptr); }();
-  const int64_t ksm = kern == 6 ? (int64_t)c->smem_ws[1][0] : kern == 4 ? (int64_t)c->smem_pipe[1][0] : (int64_t)c->smem[1][0];
-  const int64_t kgr = kern == 6 ? c->grid_ws[1][0] : kern == 4 ? c->grid_pipe[1][0] : c->grid[1][0];
+  const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : (int64_t)c->smem[1][0];
+  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : c->grid[1][0];
   const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0],
                        kern, ksm, kgr};
   for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
@@ -1109,8 +1103,7 @@ int ipdg_debug_grid_cap(ipdg_ctx c, int cap) {
 }
 
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 6 || variant == 3 || (variant == 5 && c->N > 4) || (variant == 6 && c->N > 5))
-    return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 5 || variant == 3 || (variant == 5 && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

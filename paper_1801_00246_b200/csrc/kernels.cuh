@@ -105,7 +105,6 @@ struct AxArgs {
   double* x;             // deferred update x += alpha_{k-1} p_{k-1}
   int defer_x;           // k_pipe: 1 = pass A applies the deferred x update, 0 = pass B updates x
   const double* halo_p;  // [H x NP] received ghost values of p_k (multi-GPU), else null
-  const double* zero_row; // >= 64 zeros, 16-byte aligned (k_ws: p_{k-1} of halo ghosts)
   struct PcgState* st;
   double* partials;      // [gridDim.x]
   unsigned int* counter;

@@ -611,8 +611,7 @@ static __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restr
   const double alpha = rho / sigma;
   const double* __restrict__ p = (k & 1) ? p_odd : p_even;
   double rz = 0.0, rr = 0.0;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-  auto one = [&](int64_t i) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (x) x[i] = fma(alpha, p[i], x[i]);
     const double ri = r[i] - alpha * Ap[i];
     r[i] = ri;
@@ -620,37 +619,6 @@ static __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restr
     if (dinv) z[i] = zi;
     rz += ri * zi;
     rr += ri * ri;
-  };
-  const bool vec = !x && dinv && (((uintptr_t)r | (uintptr_t)Ap | (uintptr_t)dinv | (uintptr_t)z) & 15) == 0;
-  if (vec) {
-    // streaming at the HBM roofline: 16-byte accesses, two independent pairs in flight per thread
-    const int64_t n2 = n / 2;
-    double2* r2 = reinterpret_cast<double2*>(r);
-    const double2* a2 = reinterpret_cast<const double2*>(Ap);
-    const double2* d2 = reinterpret_cast<const double2*>(dinv);
-    double2* z2 = reinterpret_cast<double2*>(z);
-    int64_t j = tid;
-    for (; j + stride < n2; j += 2 * stride) {
-      const double2 ra = r2[j], aa = a2[j], da = d2[j];
-      const double2 rb = r2[j + stride], ab = a2[j + stride], db = d2[j + stride];
-      const double2 r_a = make_double2(ra.x - alpha * aa.x, ra.y - alpha * aa.y);
-      const double2 r_b = make_double2(rb.x - alpha * ab.x, rb.y - alpha * ab.y);
-      const double2 z_a = make_double2(r_a.x * da.x, r_a.y * da.y);
-      const double2 z_b = make_double2(r_b.x * db.x, r_b.y * db.y);
-      r2[j] = r_a;
-      r2[j + stride] = r_b;
-      z2[j] = z_a;
-      z2[j + stride] = z_b;
-      rz += r_a.x * z_a.x + r_a.y * z_a.y + r_b.x * z_b.x + r_b.y * z_b.y;
-      rr += r_a.x * r_a.x + r_a.y * r_a.y + r_b.x * r_b.x + r_b.y * r_b.y;
-    }
-    for (; j < n2; j += stride) {
-      one(2 * j);
-      one(2 * j + 1);
-    }
-    if ((n & 1) && tid == 0) one(n - 1);
-  } else {
-    for (int64_t i = tid; i < n; i += stride) one(i);
   }
   double v[2] = {rz, rr}, out[2];
   if (grid_reduce<2>(v, red, partials, counter, out)) {

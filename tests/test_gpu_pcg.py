@@ -71,7 +71,7 @@ def test_jacobi_nearly_neumann_long_solve(N):
     assert np.linalg.norm(r) <= max(1e-8, true_o) * np.linalg.norm(b) * (1 + 1e-6)
 
 
-@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5), (2, 6), (3, 6), (4, 6), (5, 6)])
+@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5)])
 def test_pcg_other_kernel_variant(N, variant):
     m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=13)
     check_solve(m, N, 1, 1e-9, variant=variant)
@@ -140,7 +140,7 @@ def test_block_jacobi_needs_positive_lambda():
         op.pcg_solve(b, precond=2, lam=0.0)
 
 
-@pytest.mark.parametrize("N,variant", [(3, 4), (4, 4), (5, 4), (3, 6), (4, 6)])
+@pytest.mark.parametrize("N,variant", [(3, 4), (4, 4), (5, 4)])
 def test_split_pass_a_two_launch_reduction(N, variant):
     """The multi-GPU pass A runs interior blocks, then halo-boundary blocks after the exchange, with p.Ap
     summed over the two launches (AxArgs::red_part).  Forced on one partition (odd blocks as the second
