@@ -45,6 +45,16 @@ struct ipdg_ctx_s {
   // split variant (k_grad + k_flux): neighbour ids per element, W = [w_r | w_s] scratch
   int4* nbg = nullptr;
   double* W2 = nullptr;
+  // thread-per-element block variant (k_tpb): kTpbE consecutive elements per block, ghost faces
+  short4* nbt = nullptr;
+  int* gfoff_t = nullptr;
+  int* gface_t = nullptr;
+  double* tauF = nullptr;
+  int nblocks_t = 0, gmax_t = 0;
+  int* blist_t = nullptr;      // split pass A: [interior blocks | halo-boundary blocks]
+  int nbt_split[2] = {0, 0};
+  size_t smem_tpb_m[2] = {0, 0};  // [mode]
+  bool tpb_ok[2][2] = {{false, false}, {false, false}};  // [mode][lam] fits on an SM
   int grid_cap = 0;  // debug: cap on every persistent grid (0 = off)
   int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4), 4 pipelined fused
   // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit

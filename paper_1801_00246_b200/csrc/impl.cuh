@@ -11,6 +11,11 @@
 #include "cops.cuh"
 #include "sipdg_gather.cuh"
 #include "dgops.cuh"
+#include "sipdg_tpb.cuh"
+
+#ifndef IPDG_TPB_MAXN
+#define IPDG_TPB_MAXN 8  // highest degree with a k_tpb instantiation (lower it for quick rebuilds)
+#endif
 
 // ------------------------------------------------------------------ per-N dispatch
 template <int N>
@@ -197,7 +202,51 @@ struct Impl {
         c->grid_flux[mode][lam] = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + S::W - 1) / S::W, (int64_t)std::max(1, o) * c->sms));
       }
     }
+    TRY(configure_tpb(c, optin));
     return configure_pipe(c, optin);
+  }
+
+  static int configure_tpb(ipdg_ctx c, int optin) {
+    if constexpr (N <= IPDG_TPB_MAXN) {
+    for (int lam = 0; lam < 2; ++lam)
+      for (int mode = 0; mode < 2; ++mode) {
+        const size_t bytes = (size_t)TpbLayout<N>::total(c->gmax_t, mode == 1) * sizeof(double);
+        c->smem_tpb_m[mode] = bytes;
+        const void* fn = (mode == 0) ? (lam ? (const void*)k_tpb<N, MODE_AX, true> : (const void*)k_tpb<N, MODE_AX, false>)
+                                     : (lam ? (const void*)k_tpb<N, MODE_PCG_A, true> : (const void*)k_tpb<N, MODE_PCG_A, false>);
+        c->tpb_ok[mode][lam] = false;
+        if ((int)bytes > optin - 1024) continue;
+        CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        int occ = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TrB<N>::NTHR, bytes));
+        c->tpb_ok[mode][lam] = occ > 0;
+      }
+    }
+    return IPDG_OK;
+  }
+
+  // one CTA per block of kTpbE elements (all blocks, or the interior / boundary lists of a split pass A)
+  template <int MODE>
+  static int launch_tpb(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s, const int* list, int n) {
+    if constexpr (N > IPDG_TPB_MAXN) {
+      FAIL(c, IPDG_EINVAL, "k_tpb not built for N = %d", N);
+    } else {
+    a.nbt = c->nbt;
+    a.gfoff = c->gfoff_t;
+    a.gface = c->gface_t;
+    a.tauF = c->tauF;
+    a.blist = list;
+    a.nlist = n;
+    const int grid = list ? n : c->nblocks_t;
+    if (grid <= 0) return IPDG_OK;
+    if (MODE == MODE_PCG_A && grid > c->partials_cap) FAIL(c, IPDG_ECUDA, "partials buffer too small");
+    const size_t smb = c->smem_tpb_m[MODE == MODE_PCG_A ? 1 : 0];
+    if (lam) k_tpb<N, MODE, true><<<grid, TrB<N>::NTHR, smb, s>>>(a, c->gmax_t);
+    else k_tpb<N, MODE, false><<<grid, TrB<N>::NTHR, smb, s>>>(a, c->gmax_t);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+    }
   }
 
   // ---- pipelined fused variant: needs room for the staging area next to the working rows
@@ -229,7 +278,82 @@ struct Impl {
     return IPDG_OK;
   }
 
+  // k_tpb operator tables (sipdg_tpb.cuh): face-restricted derivative split checked against Dr / Ds
+  static int upload_tpb_constants(ipdg_ctx c) {
+    using B = TrB<N>;
+    const RefOps& R = c->ref;
+    const int NP = B::NP, NFP = B::NFP;
+    std::vector<double> h(B::TOTAL, 0.0);
+    auto D = [&](const std::vector<double>& A, int i, int j) { return A[i * NP + j]; };
+    if constexpr (B::GRAD) {
+      for (int i = 0; i < NP; ++i)
+        for (int j = 0; j < NP; ++j) {
+          h[B::O_DRT + j * NP + i] = D(R.Dr, i, j);
+          h[B::O_DST + j * NP + i] = D(R.Ds, i, j);
+          h[B::O_SR + i * NP + j] = D(R.Sr, i, j);
+          h[B::O_SS + i * NP + j] = D(R.Ss, i, j);
+        }
+    }
+    // K_rr = Dr^T M Dr, K_rs = Dr^T M Ds + Ds^T M Dr, K_ss = Ds^T M Ds (Sr = M Dr, Ss = M Ds); [j][n], symmetric
+    for (int i = 0; i < NP && !B::GRAD; ++i)
+      for (int j = 0; j < NP; ++j) {
+        double rr = 0, rs = 0, ss = 0;
+        for (int a = 0; a < NP; ++a) {
+          rr += D(R.Dr, a, i) * D(R.Sr, a, j);
+          rs += D(R.Dr, a, i) * D(R.Ss, a, j) + D(R.Ds, a, i) * D(R.Sr, a, j);
+          ss += D(R.Ds, a, i) * D(R.Ss, a, j);
+        }
+        h[B::O_KRR + i * NP + j] = rr;
+        h[B::O_KRS + i * NP + j] = rs;
+        h[B::O_KSS + i * NP + j] = ss;
+      }
+    // tangential derivative d/dxi along each face (face node order) and the transverse rows T_f
+    std::vector<double> D1D(NFP * NFP), Tf(3 * NFP * NP);
+    for (int k = 0; k < NFP; ++k)
+      for (int m = 0; m < NFP; ++m) D1D[k * NFP + m] = D(R.Dr, R.Fmask[k], R.Fmask[m]);
+    double dmax = 0.0, bad = 0.0;
+    for (double v : R.Dr) dmax = std::max(dmax, std::fabs(v));
+    for (int f = 0; f < 3; ++f)
+      for (int k = 0; k < NFP; ++k) {
+        const int i = R.Fmask[f * NFP + k];
+        for (int j = 0; j < NP; ++j) {
+          const double tang = (f == 0) ? D(R.Dr, i, j) : (f == 1) ? D(R.Ds, i, j) - D(R.Dr, i, j) : D(R.Ds, i, j);
+          double want = 0.0;
+          for (int m = 0; m < NFP; ++m)
+            if (R.Fmask[f * NFP + m] == j) want = D1D[k * NFP + m];
+          bad = std::max(bad, std::fabs(tang - want));
+          Tf[(f * NFP + k) * NP + j] = (f == 0) ? D(R.Ds, i, j) : D(R.Dr, i, j);
+          h[B::O_TN + (f * NFP + k) * NP + j] = Tf[(f * NFP + k) * NP + j];
+        }
+      }
+    if (bad > 1e-9 * dmax) FAIL(c, IPDG_ECUDA, "k_tpb: face-tangential derivative check failed (%g)", bad);
+    if constexpr (!B::BIG) {
+      for (int f = 0; f < 3; ++f)
+        for (int n = 0; n < NP; ++n)
+          for (int k = 0; k < NFP; ++k) {
+            double v = 0;
+            for (int m = 0; m < NFP; ++m) v += Tf[(f * NFP + m) * NP + n] * R.M1D[m * NFP + k];
+            h[B::O_PT + (f * NFP + k) * NP + n] = v;
+          }
+      for (int m = 0; m < NFP; ++m)
+        for (int k = 0; k < NFP; ++k) {
+          double v = 0;
+          for (int j = 0; j < NFP; ++j) v += D1D[j * NFP + m] * R.M1D[j * NFP + k];
+          h[B::O_QT + k * NFP + m] = v;
+        }
+      for (int i = 0; i < NP * NP; ++i) h[B::O_M + i] = R.M[i];
+    }
+    for (int m = 0; m < NFP; ++m)
+      for (int k = 0; k < NFP; ++k) {
+        h[B::O_M1D + m * NFP + k] = R.M1D[m * NFP + k];
+        h[B::O_D1DT + m * NFP + k] = D1D[k * NFP + m];
+      }
+    CUDA_TRY(c, cudaMemcpyToSymbol(c_tpb<N>, h.data(), h.size() * sizeof(double)));
+    return IPDG_OK;
+  }
+
   static int upload_constants(ipdg_ctx c) {
+    TRY(upload_tpb_constants(c));
     if constexpr (N <= 4) {
       using TT = TrT<N>;
       const RefOps& R = c->ref;
@@ -261,17 +385,16 @@ struct Impl {
 
   // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
-  // Kernel actually used (1 fused k_sipdg, 2 split, 3 thread-per-element, 4 pipelined k_pipe, 5 gather).
-  // Auto (variant 0), the fastest measured per degree and pass: Ax -- gather for N <= 3, pipelined fused
-  // for N = 4, 5, split for N >= 6 (C3 sweep, profiles/r01_sweep_*.jsonl); PCG pass A -- gather for N = 1,
-  // pipelined fused for N = 2..5 (its p formation and x update are cheaper in the staged kernel:
-  // tools/pcg_lowN_timing.py on C2, N = 2: 47 vs 50 us, N = 3: 68 vs 74 us), split for N >= 6.
+  // Kernel actually used (1 fused k_sipdg, 2 split, 4 pipelined k_pipe, 5 gather, 6 thread-per-element
+  // block k_tpb).  Auto (variant 0), the fastest measured per degree on C3 (profiles/r02_c3_variants.jsonl):
+  // k_tpb for N <= 3 (Ax and PCG pass A), pipelined fused for N = 4, 5, split for N >= 6.
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : (N <= (mode == 0 ? 3 : 1) ? 5 : 4);
+    if (k == 0) k = (N >= 6) ? 2 : (N <= 3 ? 6 : 4);
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
+    if (k == 6 && !(c->tpb_ok[mode][lam] && (!lam || TrB<N>::HAS_LAM) && (v == nullptr || aligned16(v)))) k = 1;
     if (k == 4 && !(c->grid_pipe[mode][lam] > 0 && aligned16(v))) k = 1;
     return k;
   }
@@ -413,6 +536,10 @@ struct Impl {
     a.Au = Au;
     a.lambda = lambda;
     if (k == 5) return launch_gather<MODE_AX>(c, a, lam, s);
+    if (k == 6) {
+      if (!aligned16(Au)) FAIL(c, IPDG_EINVAL, "k_tpb: Au must be 16-byte aligned");
+      return launch_tpb<MODE_AX>(c, a, lam, s, nullptr, 0);
+    }
     if (k == 4) {
       const int gp = c->grid_pipe[0][lam];
       if (lam) k_pipe<N, MODE_AX, true><<<gp, T::W * 32, c->smem_pipe[0][1], s>>>(a, c->gmax);
@@ -447,6 +574,19 @@ struct Impl {
     a.counter = c->counter;
     const bool lam = c->lambda != 0.0;
     if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
+    if (k == 6) {
+      a.defer_x = 1;
+      if (c->split_a) {  // interior blocks, (wait for the halo exchange), halo-boundary blocks
+        const int ni = c->nbt_split[0], nbd = c->nbt_split[1];
+        a.red_part = (ni > 0 && nbd > 0) ? 1 : 0;
+        if (ni > 0) TRY(launch_tpb<MODE_PCG_A>(c, a, lam, s, c->blist_t, ni));
+        if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
+        a.red_part = (ni > 0 && nbd > 0) ? 2 : 0;
+        if (nbd > 0) TRY(launch_tpb<MODE_PCG_A>(c, a, lam, s, c->blist_t + ni, nbd));
+        return IPDG_OK;
+      }
+      return launch_tpb<MODE_PCG_A>(c, a, lam, s, nullptr, 0);
+    }
     if (k == 4) {
       const int gp = c->grid_pipe[1][lam];
       auto launch = [&](int part, const int* list, int n) -> int {

@@ -82,9 +82,12 @@ static void free_mesh(ipdg_ctx c) {
   if (c->hostio) cudaFree(c->hostio);
   c->hostio = nullptr;
   c->hostio_n = 0;
-  void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2};
+  void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
+                  c->nbt, c->gfoff_t, c->gface_t, c->tauF, c->blist_t};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  c->nbt = nullptr; c->gfoff_t = nullptr; c->gface_t = nullptr; c->tauF = nullptr; c->blist_t = nullptr;
+  c->nblocks_t = 0; c->gmax_t = 0;
   c->geo = nullptr; c->gG = nullptr; c->gF = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
   c->nbg = nullptr; c->W2 = nullptr;
   c->bcode = nullptr;
@@ -363,6 +366,82 @@ static int build_block_lists(ipdg_ctx c, int64_t K, const std::vector<int>& boff
   return IPDG_OK;
 }
 
+// k_tpb schedule: blocks of kTpbE consecutive elements (one thread each).  Per own face a slot: the
+// neighbour's position in the block (own element), kTpbE + g for the block's g-th ghost face (neighbour
+// outside the block, incl. halo ghosts >= K), or the element itself on a boundary face; flags as nbr.
+// Ghost faces are listed per block as (neighbour << 2) | neighbour's face, sorted by that face so that
+// the recomputation of their traces stays warp-convergent.  The split pass A lists (interior blocks,
+// then blocks with a halo ghost face) follow build_block_lists.
+static int build_tpb(ipdg_ctx c, int64_t K, const std::vector<int>& etoe, const std::vector<int>& etof, const int8_t* bc) {
+  const int E = kTpbE;
+  const int nb = (int)((K + E - 1) / E);
+  std::vector<short4> nbt(K);
+  std::vector<int> gfoff(1, 0), gface;
+  std::vector<int> in, bd;
+  int gmax = 0;
+  std::vector<std::pair<int, int>> gl;  // (face', neighbour) of this block's ghost faces, own face order
+  std::vector<int> own_ref;             // per ghost entry: own element * 3 + face
+  for (int b = 0; b < nb; ++b) {
+    const int64_t e0 = (int64_t)b * E, e1 = std::min<int64_t>(K, e0 + E);
+    gl.clear();
+    own_ref.clear();
+    for (int64_t e = e0; e < e1; ++e)
+      for (int f = 0; f < 3; ++f) {
+        const int n = etoe[e * 3 + f];
+        if (n >= 0 && (n < e0 || n >= e1)) {
+          gl.push_back({etof[e * 3 + f], (int)own_ref.size()});
+          own_ref.push_back((int)(e * 3 + f));
+        }
+      }
+    std::stable_sort(gl.begin(), gl.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first < y.first; });
+    std::vector<int> gslot(own_ref.size());
+    bool halo = false;
+    for (size_t g = 0; g < gl.size(); ++g) {
+      const int ef = own_ref[gl[g].second];
+      const int n = etoe[ef];
+      halo |= n >= K;
+      gface.push_back((n << 2) | gl[g].first);
+      gslot[gl[g].second] = E + (int)g;
+    }
+    gmax = std::max(gmax, (int)gl.size());
+    gfoff.push_back((int)gface.size());
+    if (c->force_split ? (b & 1) : halo) bd.push_back(b);
+    else in.push_back(b);
+    size_t gi = 0;
+    for (int64_t e = e0; e < e1; ++e) {
+      short sl[3];
+      int flags = 0;
+      for (int f = 0; f < 3; ++f) {
+        const int n = etoe[e * 3 + f];
+        int slot = (int)(e - e0);
+        if (n >= 0) slot = (n >= e0 && n < e1) ? (int)(n - e0) : gslot[gi++];
+        sl[f] = (short)slot;
+        const int fp = n >= 0 ? etof[e * 3 + f] : 0;
+        const int code = (bc[e * 3 + f] == IPDG_BC_REMOTE) ? IPDG_BC_INTERIOR : bc[e * 3 + f];
+        flags |= ((fp & 3) | ((code & 3) << 2)) << (4 * f);
+      }
+      nbt[e] = make_short4(sl[0], sl[1], sl[2], (short)flags);
+    }
+  }
+  if (E + gmax > 32000 || (K + c->H) >= (1ll << 29)) FAIL(c, IPDG_EMESH, "k_tpb schedule: %d ghost faces in a block", gmax);
+  c->nblocks_t = nb;
+  c->gmax_t = gmax;
+  c->nbt_split[0] = (int)in.size();
+  c->nbt_split[1] = (int)bd.size();
+  in.insert(in.end(), bd.begin(), bd.end());
+  if (gface.empty()) gface.push_back(0);
+  TRY(upload(c, &c->nbt, nbt.data(), nbt.size()));
+  TRY(upload(c, &c->gfoff_t, gfoff.data(), gfoff.size()));
+  TRY(upload(c, &c->gface_t, gface.data(), gface.size()));
+  TRY(upload(c, &c->blist_t, in.data(), in.size()));
+  return IPDG_OK;
+}
+
+__global__ void k_tauf(int64_t K, const double* __restrict__ gF, double* __restrict__ tauF) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < K * 3) tauF[i] = gF[(i / 3) * kGF + 3 * (i % 3) + 2];
+}
+
 // debug grid cap (ipdg_debug_grid_cap): clamp every persistent grid so that small test meshes run
 // several element blocks per CTA (the prefetch / ring paths of the pipelined kernels)
 static void apply_grid_cap(ipdg_ctx c) {
@@ -433,6 +512,10 @@ static int finalize_mesh(ipdg_ctx c, int64_t H, const double* ghost_vxy) {
   CUDA_TRY(c, cudaMalloc(&c->gG, KH * sizeof(double4)));
   CUDA_TRY(c, cudaMalloc(&c->gF, std::max<int64_t>(1, K) * kGF * sizeof(double)));
   k_geofacs<<<(unsigned)((KH + 255) / 256), 256>>>(K, KH, c->geo, c->etoe, c->bcode, c->tau_c, c->gG, c->gF);
+  c->launches++;
+  TRY(build_tpb(c, K, etoe, etof, bc));
+  CUDA_TRY(c, cudaMalloc(&c->tauF, std::max<int64_t>(1, K) * 3 * sizeof(double)));
+  k_tauf<<<(unsigned)((K * 3 + 255) / 256), 256>>>(K, c->gF, c->tauF);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   TRY(impl_ops(c->N)->configure(c));
@@ -672,7 +755,8 @@ static int ensure_ws(ipdg_ctx c) {
 
 static int ensure_partials(ipdg_ctx c) {
   // one slot per CTA of the largest reducing grid (k_gather: one CTA per kGatherThreads elements)
-  const int need = (int)std::max<int64_t>(std::max(4096, 4 * c->sms * 16), (c->K + kGatherThreads - 1) / kGatherThreads);
+  const int need = (int)std::max<int64_t>(std::max<int64_t>(std::max(4096, 4 * c->sms * 16), (c->K + kGatherThreads - 1) / kGatherThreads),
+                                           c->nblocks_t);
   if (c->partials && c->partials_cap >= need) return IPDG_OK;
   if (c->partials) cudaFree(c->partials);
   CUDA_TRY(c, cudaMalloc(&c->partials, 3 * sizeof(double) * need));
@@ -720,7 +804,7 @@ static int resolved_pass_a(ipdg_ctx c) {
 
 static int one_iteration(ipdg_ctx c, cudaStream_t s) {
   const int kern = resolved_pass_a(c);
-  if (c->split_a && (kern == 4 || (kern == 2 && c->H > 0))) {
+  if (c->split_a && (kern == 4 || kern == 6 || (kern == 2 && c->H > 0))) {
     // halo exchange of p_k on the comm stream, overlapping the interior blocks of pass A
     c->halo_ev_pending = false;
     if ((c->H > 0 || c->S > 0) && !c->halo_external) {
@@ -1044,8 +1128,8 @@ int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   if (!c || !out) return IPDG_EINVAL;
   // resolved pass-A kernel for lambda = 0 and its launch shape
   const int kern = [&]() -> int { return impl_ops(c->N)->resolve(c, 1, false, nullptr); }();
-  const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : (int64_t)c->smem[1][0];
-  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : c->grid[1][0];
+  const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : kern == 6 ? (int64_t)c->smem_tpb_m[1] : (int64_t)c->smem[1][0];
+  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : kern == 6 ? c->nblocks_t : c->grid[1][0];
   const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0],
                        kern, ksm, kgr};
   for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
@@ -1081,6 +1165,7 @@ int ipdg_debug_split_pass_a(ipdg_ctx c, int on) {
   std::vector<int> gid(std::max(1, goff.back()));
   if (goff.back() > 0) CUDA_TRY(c, cudaMemcpy(gid.data(), c->gid, goff.back() * sizeof(int), cudaMemcpyDeviceToHost));
   TRY(build_block_lists(c, c->K, boff, goff, gid));
+  TRY(build_tpb(c, c->K, c->etoe_h, c->etof_h, c->pend_bc.data()));
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   c->gkey_x = nullptr;
@@ -1103,7 +1188,7 @@ int ipdg_debug_grid_cap(ipdg_ctx c, int cap) {
 }
 
 int ipdg_set_variant(ipdg_ctx c, int variant) {
-  if (!c || variant < 0 || variant > 5 || variant == 3 || (variant == 5 && c->N > 4)) return IPDG_EINVAL;
+  if (!c || variant < 0 || variant > 6 || variant == 3 || (variant == 5 && c->N > 4)) return IPDG_EINVAL;
   c->variant = variant;
   for (auto& g : c->gexec)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }

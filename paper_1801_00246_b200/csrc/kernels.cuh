@@ -108,7 +108,18 @@ struct AxArgs {
   struct PcgState* st;
   double* partials;      // [gridDim.x]
   unsigned int* counter;
+  // k_tpb (thread per element, blocks of kTpbE consecutive elements)
+  const short4* nbt;     // [K] per face: slot (own e - e0 < kTpbE, ghost face kTpbE + g, boundary: own) + flags as nbr
+  const int* gfoff;      // [nblocks_t + 1] ghost-face list offsets
+  const int* gface;      // ghost faces: (neighbour element << 2) | its face, sorted by face within a block
+  const double* tauF;    // [K x 3] sJ tau per face
 };
+
+// k_tpb: elements per CTA (block of consecutive elements)
+#ifndef IPDG_TPB_E
+#define IPDG_TPB_E 128
+#endif
+constexpr int kTpbE = IPDG_TPB_E;
 
 // Device-side PCG state (one per context).  See ipdg.cu "PCG protocol".
 struct PcgState {

@@ -18,7 +18,7 @@ def _mesh():
                           tag=lambda x, y: np.where(y > 0.4, 1, 2).astype(np.int8))
 
 
-@pytest.mark.parametrize("N,variant", [(1, 1), (4, 1), (6, 1), (8, 1), (1, 2), (4, 2), (6, 2), (8, 2), (2, 4), (4, 4), (6, 4), (1, 5), (2, 5)])
+@pytest.mark.parametrize("N,variant", [(1, 1), (4, 1), (6, 1), (8, 1), (1, 2), (4, 2), (6, 2), (8, 2), (2, 4), (4, 4), (6, 4), (1, 5), (2, 5), (1, 6), (3, 6), (4, 6), (8, 6)])
 @pytest.mark.parametrize("P", [2, 3])
 def test_partitioned_ax_loopback(N, P, variant):
     m = _mesh()

@@ -44,7 +44,7 @@ def ax_oracle(N):
     return assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref), mass_matrix(m["VX"], m["VY"], m["EToV"], ref)
 
 
-AX_CASES = [(N, v) for N in range(1, 9) for v in (0, 1, 2, 4, 5) if v != 5 or N <= 4]
+AX_CASES = [(N, v) for N in range(1, 9) for v in (0, 1, 2, 4, 5, 6) if v != 5 or N <= 4]
 
 
 @pytest.mark.parametrize("cap", [1, 3])
@@ -81,7 +81,7 @@ def pcg_problem(N, precond):
     return m, A, b, lam, tol, st["iterations"], tuple(counts), true_o
 
 
-PCG_CASES = [(N, p, v) for N in range(1, 9) for p in (0, 1, 2) for v in (0, 1, 2, 4, 5)
+PCG_CASES = [(N, p, v) for N in range(1, 9) for p in (0, 1, 2) for v in (0, 1, 2, 4, 5, 6)
              if v != 5 or N <= 4]
 
 

@@ -153,10 +153,11 @@ def test_full_size_c2_parity(N):
     assert err.max() <= 1e-11
 
 
-@pytest.mark.parametrize("N,variant", [(N, v) for N in range(1, 9) for v in (1, 2, 4, 5) if v != 5 or N <= 4])
+@pytest.mark.parametrize("N,variant", [(N, v) for N in range(1, 9) for v in (1, 2, 4, 5, 6) if v != 5 or N <= 4])
 def test_ax_kernel_variants(N, variant):
-    """Fused k_sipdg (variant 1), split k_grad + k_flux (variant 2), the pipelined fused k_pipe (variant 4)
-    and the gather kernel k_gather (variant 5, N <= 4) all match the oracle."""
+    """Fused k_sipdg (variant 1), split k_grad + k_flux (variant 2), the pipelined fused k_pipe (variant 4),
+    the gather kernel k_gather (variant 5, N <= 4) and the thread-per-element block kernel k_tpb (variant 6)
+    all match the oracle."""
     m = MESHES["mixed_bc"]()
     ref = RefElem(N)
     op = Ipdg(N, m)
@@ -168,7 +169,8 @@ def test_ax_kernel_variants(N, variant):
         assert rel(Au.ravel(), A @ u.ravel()) <= TOL, (N, variant, lam)
 
 
-@pytest.mark.parametrize("N,variant", [(1, 4), (2, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5), (2, 2), (7, 2), (3, 1)])
+@pytest.mark.parametrize("N,variant", [(1, 4), (2, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5), (2, 2), (7, 2), (3, 1),
+                                       (1, 6), (3, 6), (4, 6), (6, 6), (8, 6)])
 @pytest.mark.parametrize("mesh", ["random_order", "ragged", "tiny"])
 def test_ax_variant_meshes(N, variant, mesh):
     """The pipelined k_pipe (variant 4), k_gather (5), the split pair (2) and k_sipdg (1) on scattered
@@ -185,7 +187,7 @@ def test_ax_variant_meshes(N, variant, mesh):
 def test_bad_variants_rejected():
     m = MESHES["tiny"]()
     op = Ipdg(5, m)
-    for v in (3, 5, 6, -1):  # 3: the retired thread-per-element kernel; 5: gather needs N <= 4
+    for v in (3, 5, 7, -1):  # 3: the retired thread-per-element kernel; 5: gather needs N <= 4; 7: none
         with pytest.raises(IpdgError):
             op.set_variant(v)
 

@@ -71,7 +71,8 @@ def test_jacobi_nearly_neumann_long_solve(N):
     assert np.linalg.norm(r) <= max(1e-8, true_o) * np.linalg.norm(b) * (1 + 1e-6)
 
 
-@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5)])
+@pytest.mark.parametrize("N,variant", [(2, 2), (4, 2), (7, 1), (8, 1), (1, 4), (3, 4), (4, 4), (5, 4), (6, 4), (8, 4), (1, 5), (2, 5), (3, 5),
+                                       (1, 6), (3, 6), (4, 6), (8, 6)])
 def test_pcg_other_kernel_variant(N, variant):
     m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=13)
     check_solve(m, N, 1, 1e-9, variant=variant)
