@@ -143,6 +143,17 @@ int ipdg_pcg_solve_host(ipdg_ctx ctx, const double* b_host, double* x_host, doub
  * (same vertex numbering on every rank), and the PCG dot products are all-reduced. */
 int ipdg_comm_init(ipdg_ctx ctx, const void* nccl_unique_id, int nranks, int rank);
 
+/* Single-process loopback of the distributed PCG (tests; P:219 PCG with P:382 distribution):
+ * cs[0..P-1] are contexts on ONE device holding the partitions of one mesh, each completed by
+ * ipdg_upload_halo with neighbour ranks that index cs (no ipdg_comm_init).  b[p], x[p] are device
+ * vectors of context p (K_p x Np; x[p] holds x0 on entry, the solution on return).  Every step of the
+ * NCCL path runs in lockstep on `stream` -- p_k packing with pass A's decisions, halo exchange as
+ * device-to-device copies in the plans' order, pass A (interior / halo-boundary launches and the
+ * two-part p.Ap reduction), pass B -- and each NCCL all-reduce is a fixed-order sum over the P device
+ * states.  stats[p] (optional, P entries) as ipdg_pcg_solve.  Returns as ipdg_pcg_solve; blocks. */
+int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double* const* x, double lambda,
+                            int precond, double tol, int64_t maxit, ipdg_stats* stats, void* stream);
+
 /* Complete a mesh uploaded with IPDG_BC_REMOTE faces (multi-GPU partition, built e.g. by
  * paper_1801_00246_b200.partition.split).  HOST arrays, copied:
  *   H              ghost elements owned by other ranks (local ids K .. K+H-1)

@@ -265,6 +265,23 @@ class Ipdg:
         return int(lib().ipdg_launch_count(self.ctx))
 
 
+def loopback_pcg_solve(ops, bs, xs, lam=0.0, precond=1, tol=1e-8, maxit=10000, stream=None):
+    """Distributed PCG over the partitions `ops` (Ipdg.from_rank_mesh contexts on one device, no NCCL)
+    in lockstep: halo exchange by device copies, all-reduces by fixed-order sums (ipdg_loopback_pcg_solve).
+    bs, xs: per-partition device tensors (xs hold x0, overwritten).  Returns per-partition stats."""
+    P = len(ops)
+    for op in ops:
+        op._workspace()
+    ctxs = (ctypes.c_void_p * P)(*[op.ctx.value for op in ops])
+    bp = (ctypes.c_void_p * P)(*[b.data_ptr() for b in bs])
+    xp = (ctypes.c_void_p * P)(*[x.data_ptr() for x in xs])
+    st = (ipdg_stats * P)()
+    rc = lib().ipdg_loopback_pcg_solve(ctxs, P, bp, xp, float(lam), int(precond), float(tol), int(maxit), st,
+                                       _stream(stream))
+    check(rc, ops[0].ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
+    return [dict(iterations=s.iterations, rel_residual=s.rel_residual, bnorm=s.bnorm, status=s.status) for s in st]
+
+
 def nccl_unique_id():
     n = lib().ipdg_nccl_id_bytes()
     buf = ctypes.create_string_buffer(n)

@@ -847,14 +847,15 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
   return IPDG_OK;
 }
 
-int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, void* stream) {
+// PCG setup shared by ipdg_pcg_begin and the loopback group solve: argument checks, workspace, Jacobi
+// diagonal, device state (no Ax, no iteration graphs)
+static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, bool dir,
+                     cudaStream_t s) {
   if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || precond < 0 || precond > 2) return IPDG_EINVAL;
   if (precond == IPDG_PRECOND_BLOCK_JACOBI && !(lambda > 0.0))
     FAIL(c, IPDG_EINVAL, "block-Jacobi (scaled inverse mass) preconditioning needs lambda > 0");
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
-  const bool dir = (c->H > 0 || c->S > 0) ? c->has_dirichlet_global : c->has_dirichlet;
   if (lambda == 0.0 && !dir) FAIL(c, IPDG_ESINGULAR, "lambda = 0 and no Dirichlet face");
-  cudaStream_t s = (cudaStream_t)stream;
   TRY(ensure_ws(c));
   TRY(ensure_partials(c));
   const int64_t n = c->K * c->ref.Np;
@@ -862,7 +863,7 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
     TRY(upload(c, &c->Minv, c->ref.Minv.data(), c->ref.Minv.size()));
   }
   if (precond == IPDG_PRECOND_JACOBI && !(c->dinv_valid && c->dinv_lambda == lambda)) {
-    TRY(ipdg_diag(c, c->dinv, lambda, stream));
+    TRY([&]() -> int { DISPATCH(c->N, diag(c, c->dinv, lambda, s)); }());
     k_recip<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, c->dinv);
     c->launches++;
     c->dinv_valid = true;
@@ -871,11 +872,7 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   c->x = x;
   c->lambda = lambda;
   c->precond = precond;
-  // x is updated by pass A (deferred x += alpha_{k-1} p_{k-1}) -- measured faster on C2 than x += alpha_k p_k
-  // in pass B (pass B 18 -> 29 us, pass A -3 us) -- unless k_pipe would lose a resident CTA per SM to the
-  // x staging buffer (e.g. the lambda variant at N = 4), then pass B updates x.
-  c->xb = impl_ops(c->N)->resolve(c, 1, lambda != 0.0, x) == 4
-           && c->pipe_xb[lambda != 0.0];
+  c->xb = impl_ops(c->N)->resolve(c, 1, lambda != 0.0, x) == 4 && c->pipe_xb[lambda != 0.0];
   PcgState h;
   std::memset(&h, 0, sizeof(h));
   h.tol2 = tol * tol;
@@ -884,15 +881,26 @@ int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   h.precond = precond;
   *c->st_host = h;
   CUDA_TRY(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  return IPDG_OK;
+}
+
+// r = b - A x (A x already in c->Ap), z, partial (r.z, r.r, b.b) -> st->red_B (before the all-reduce)
+static int pcg_init_residual(ipdg_ctx c, const double* b, cudaStream_t s) {
+  if (c->precond == IPDG_PRECOND_BLOCK_JACOBI) DISPATCH(c->N, pass_b_bj(c, true, b, s));
+  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, b, c->Ap, c->r, c->precond ? c->dinv : nullptr, c->zb, c->st,
+                                         c->partials, c->counter);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+int ipdg_pcg_begin(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, void* stream) {
+  if (!c) return IPDG_EINVAL;
+  const bool dir = (c->H > 0 || c->S > 0) ? c->has_dirichlet_global : c->has_dirichlet;
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(pcg_setup(c, b, x, lambda, precond, tol, dir, s));
   TRY(ipdg_ax(c, x, c->Ap, lambda, stream));
-  if (precond == IPDG_PRECOND_BLOCK_JACOBI) {
-    TRY([&]() -> int { DISPATCH(c->N, pass_b_bj(c, true, b, s)); }());
-  } else {
-    k_pcg_init<<<vec_grid(c), 256, 0, s>>>(n, b, c->Ap, c->r, precond ? c->dinv : nullptr, c->zb, c->st, c->partials,
-                                           c->counter);
-    c->launches++;
-    CUDA_TRY(c, cudaGetLastError());
-  }
+  TRY(pcg_init_residual(c, b, s));
   TRY(allreduce(c, c->st->red_B, 3, s));
   // (re)capture the iteration graphs when the operands changed
   if (c->gkey_x != (const void*)x || c->gkey_lambda != lambda || c->gkey_precond != precond || !c->gexec[0]) {
@@ -1043,6 +1051,121 @@ int ipdg_pcg_solve_host(ipdg_ctx c, const double* b_host, double* x_host, double
   if (rc < 0) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(x_host, xd, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
+  return rc;
+}
+
+// ---- single-process loopback of the distributed PCG (tests; SURVEY T4'): P contexts on one device hold
+// the partitions of one mesh (ipdg_upload_halo plans whose neighbour ranks index `cs`).  The driver runs
+// every step of the NCCL path in lockstep on one stream -- p_k packing with pass A's decisions (k_pack_p),
+// the halo exchange (device-to-device copies from each sender's send buffer into the receivers' halo
+// buffers, in the plans' order), pass A (interior / halo-boundary launches with the two-part p.Ap
+// reduction when the halo split is active), pass B -- and replaces each NCCL all-reduce by a fixed-order
+// sum over the P device states.
+__global__ void k_group_sum(PcgState* const* sts, int P, int which, int n) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int j = 0; j < n; ++j) {
+    double v = 0.0;
+    for (int p = 0; p < P; ++p) v += (which == 0 ? &sts[p]->red_A : sts[p]->red_B)[j];
+    for (int p = 0; p < P; ++p) (which == 0 ? &sts[p]->red_A : sts[p]->red_B)[j] = v;
+  }
+}
+
+static int loop_exchange(ipdg_ctx* cs, int P, cudaStream_t s) {
+  for (int r = 0; r < P; ++r) {
+    ipdg_ctx c = cs[r];
+    const int NP = c->ref.Np;
+    for (size_t j = 0; j < c->nbr_rank.size(); ++j) {
+      const int q = c->nbr_rank[j];
+      if (q < 0 || q >= P || q == r) FAIL(c, IPDG_EINVAL, "loopback: neighbour rank %d outside the group", q);
+      ipdg_ctx src = cs[q];
+      size_t jj = 0;
+      while (jj < src->nbr_rank.size() && src->nbr_rank[jj] != r) ++jj;
+      if (jj == src->nbr_rank.size()) FAIL(c, IPDG_EMESH, "loopback: rank %d does not list rank %d", q, r);
+      const int64_t n = src->send_off[jj + 1] - src->send_off[jj], rn = c->recv_off[j + 1] - c->recv_off[j];
+      if (n != rn) FAIL(c, IPDG_EMESH, "loopback: rank %d sends %lld rows, rank %d expects %lld", q, (long long)n, r, (long long)rn);
+      if (n)
+        CUDA_TRY(c, cudaMemcpyAsync(c->halobuf + c->recv_off[j] * NP, src->sendbuf + src->send_off[jj] * NP,
+                                    n * NP * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return IPDG_OK;
+}
+
+int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double* const* x, double lambda, int precond,
+                            double tol, int64_t maxit, ipdg_stats* stats, void* stream) {
+  if (!cs || P < 1 || !b || !x || maxit < 0) return IPDG_EINVAL;
+  for (int p = 0; p < P; ++p)
+    if (!cs[p] || cs[p]->N != cs[0]->N || cs[p]->device != cs[0]->device || !b[p] || !x[p]) return IPDG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  bool dir = false;
+  for (int p = 0; p < P; ++p) dir |= cs[p]->has_dirichlet;
+  for (int p = 0; p < P; ++p) {
+    ipdg_ctx c = cs[p];
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    c->has_dirichlet_global = dir;
+    TRY(pcg_setup(c, b[p], x[p], lambda, precond, tol, dir, s));
+    c->halo_ev_pending = false;
+  }
+  PcgState** dsts = nullptr;
+  {
+    std::vector<PcgState*> h(P);
+    for (int p = 0; p < P; ++p) h[p] = cs[p]->st;
+    CUDA_TRY(cs[0], cudaMalloc(&dsts, P * sizeof(PcgState*)));
+    CUDA_TRY(cs[0], cudaMemcpy(dsts, h.data(), P * sizeof(PcgState*), cudaMemcpyHostToDevice));
+  }
+  auto run = [&]() -> int {
+    // r = b - A x0 with x0's halo
+    for (int p = 0; p < P; ++p) {
+      ipdg_ctx c = cs[p];
+      const int64_t n = c->S * c->ref.Np;
+      if (n) {
+        k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, x[p], c->sendbuf);
+        c->launches++;
+      }
+    }
+    TRY(loop_exchange(cs, P, s));
+    for (int p = 0; p < P; ++p) {
+      ipdg_ctx c = cs[p];
+      TRY([&]() -> int { DISPATCH(c->N, ax(c, x[p], c->Ap, lambda, s)); }());
+      TRY(pcg_init_residual(c, b[p], s));
+    }
+    k_group_sum<<<1, 1, 0, s>>>(dsts, P, 1, 3);
+    for (int p = 0; p < P; ++p) TRY(set_maxit(cs[p], maxit, s));
+    int64_t done = 0;
+    while (done <= maxit) {
+      const int64_t chunk = std::min<int64_t>(kChunk, maxit + 1 - done);
+      for (int64_t it = 0; it < chunk; ++it) {
+        for (int p = 0; p < P; ++p) {
+          ipdg_ctx c = cs[p];
+          const int64_t n = c->S * c->ref.Np;
+          if (n) {
+            k_pack_p<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->S, c->ref.Np, c->send_idx, c->precond ? c->zb : c->r,
+                                                                 c->pe, c->po, c->st, c->sendbuf);
+            c->launches++;
+          }
+        }
+        TRY(loop_exchange(cs, P, s));
+        for (int p = 0; p < P; ++p) TRY([&]() -> int { DISPATCH(cs[p]->N, pass_a(cs[p], s)); }());
+        k_group_sum<<<1, 1, 0, s>>>(dsts, P, 0, 1);
+        for (int p = 0; p < P; ++p) TRY(pass_b(cs[p], s));
+        k_group_sum<<<1, 1, 0, s>>>(dsts, P, 1, 2);
+        CUDA_TRY(cs[0], cudaGetLastError());
+      }
+      done += chunk;
+      ipdg_ctx c0 = cs[0];
+      CUDA_TRY(c0, cudaMemcpyAsync(&c0->st_host->stop_iter, &c0->st->stop_iter, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(c0, cudaStreamSynchronize(s));
+      if (c0->st_host->stop_iter >= 0) break;
+    }
+    for (int p = 0; p < P; ++p) {
+      const int rc = ipdg_pcg_end(cs[p], stats ? &stats[p] : nullptr, stream);
+      if (rc < 0) return rc;
+      if (p == P - 1) return rc;
+    }
+    return IPDG_OK;
+  };
+  const int rc = run();
+  cudaFree(dsts);
   return rc;
 }
 

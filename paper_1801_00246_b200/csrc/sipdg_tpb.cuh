@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     pnew = (d.k & 1) ? a.p_odd : a.p_even;
     pold = (d.k & 1) ? a.p_even : a.p_odd;
     U = a.z;
-    if (d.stop) {  // every CTA applies the deferred x update to its own rows
-      const int64_t lo = (int64_t)b * E * NP, hi = min((int64_t)(b + 1) * E, K) * NP;
-      for (int64_t i = lo + tid; i < hi; i += NTHR) {
+    if (d.stop) {  // the deferred x update of ALL rows (grid-stride): a split pass A stops in its first launch
+      const int64_t n = K * NP;
+      for (int64_t i = blockIdx.x * (int64_t)NTHR + tid; i < n; i += (int64_t)gridDim.x * NTHR) {
         if (d.zero_x) a.x[i] = 0.0;
         else if (d.do_xupd && a.defer_x) a.x[i] += d.alpha_prev * pold[i];
       }
@@ -290,21 +290,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   if (bulk) mbar_wait(mbar, 0);
   cp_async_wait_all();
   __syncthreads();
-  if (PCG) {  // p_k = z + beta p_{k-1} in place, p_k and the deferred x update x += alpha_{k-1} p_{k-1}
-    const double alpha_prev = d.alpha_prev;
-#pragma unroll
-    for (int i = 0; i < XQ; ++i) {
-      const int q = tid + i * NTHR;
-      if (q < nrow) {
-        const double po = with_p ? spo[q] : 0.0;
-        const double v = with_p ? fma(beta, po, rows[q]) : rows[q];
-        rows[q] = v;
-        pnew[g0 + q] = v;
-        if (with_x) a.x[g0 + q] = fma(alpha_prev, po, xr[i]);
-      }
-    }
-    __syncthreads();  // p_k rows complete before the own-element phase reads them
-  }
   // ---- ghost faces: value and trace of the outside neighbour on the shared face (rows from smem;
   // PCG: p_k = z + beta p_{k-1}, the same FMA as the owner's)
   for (int g = tid; g < ((IPDG_TPB_SKIP & 1) ? 0 : Gb); g += NTHR) {
@@ -320,6 +305,22 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     else if (fp == 1) ghost_face<N, 1>(un, gq, go);
     else ghost_face<N, 2>(un, gq, go);
   }
+
+  if (PCG) {  // p_k = z + beta p_{k-1} in place, p_k and the deferred x update x += alpha_{k-1} p_{k-1}
+    const double alpha_prev = d.alpha_prev;
+#pragma unroll
+    for (int i = 0; i < XQ; ++i) {
+      const int q = tid + i * NTHR;
+      if (q < nrow) {
+        const double po = with_p ? spo[q] : 0.0;
+        const double v = with_p ? fma(beta, po, rows[q]) : rows[q];
+        rows[q] = v;
+        pnew[g0 + q] = v;
+        if (with_x) a.x[g0 + q] = fma(alpha_prev, po, xr[i]);
+      }
+    }
+  }
+  __syncthreads();  // p_k rows complete; ghost rows consumed before the face records overwrite them
 
   // ---- own elements (R per thread: slots tid + r NTHR): volume, own face values and traces.  Outer
   // products: NP independent accumulators per element, every constant feeds R FMAs.

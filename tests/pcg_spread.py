@@ -5,15 +5,19 @@ import numpy as np
 from oracle import solvers
 
 
-def oracle_iteration_spread(A, b, tol, maxit, precond, lam, ref, m, seeds=(1, 2, 3, 4, 5)):
+def oracle_iteration_spread(A, b, tol, maxit, precond, lam, ref, m, seeds=(1, 2, 3, 4, 5), true_res=None):
     """Oracle PCG iteration counts on the system as given and under random symmetric permutations of the
     unknowns (P A P^T, P b): the same mathematics with every sum in a different order.  Returns (x of the
-    unpermuted solve, its stats, the sorted list of counts)."""
+    unpermuted solve, its stats, the sorted list of counts).  With a list `true_res`, appends the true
+    relative residual ||b - A x|| / ||b|| of every sample (the rounding drift of the recursive residual)."""
     n = b.size
     dinv = 1.0 / A.diagonal() if precond == 1 else None
     Pb = solvers.inverse_mass_preconditioner(m["VX"], m["VY"], m["EToV"], ref, lam) if precond == 2 else None
     x, st = solvers.pcg(lambda v: A @ v, b, tol, maxit, dinv=dinv, apply_P=Pb)
     counts = [st["iterations"]]
+    nb = np.linalg.norm(b)
+    if true_res is not None:
+        true_res.append(np.linalg.norm(b - A @ x) / nb)
     for seed in seeds:
         perm = np.random.default_rng(seed).permutation(n)
         inv = np.empty_like(perm)
@@ -24,8 +28,10 @@ def oracle_iteration_spread(A, b, tol, maxit, precond, lam, ref, m, seeds=(1, 2,
                 return Pb(r[inv])[perm]
         else:
             P = None
-        _, sp = solvers.pcg(lambda v: Ap @ v, b[perm], tol, maxit, dinv=None if dinv is None else dinv[perm], apply_P=P)
+        xp, sp = solvers.pcg(lambda v: Ap @ v, b[perm], tol, maxit, dinv=None if dinv is None else dinv[perm], apply_P=P)
         counts.append(sp["iterations"])
+        if true_res is not None:
+            true_res.append(np.linalg.norm(b[perm] - Ap @ xp) / nb)
     return x, st, sorted(counts)
 
 

@@ -141,7 +141,7 @@ def test_block_jacobi_needs_positive_lambda():
         op.pcg_solve(b, precond=2, lam=0.0)
 
 
-@pytest.mark.parametrize("N,variant", [(3, 4), (4, 4), (5, 4)])
+@pytest.mark.parametrize("N,variant", [(3, 4), (4, 4), (5, 4), (1, 6), (3, 6), (4, 6), (8, 6)])
 def test_split_pass_a_two_launch_reduction(N, variant):
     """The multi-GPU pass A runs interior blocks, then halo-boundary blocks after the exchange, with p.Ap
     summed over the two launches (AxArgs::red_part).  Forced on one partition (odd blocks as the second
