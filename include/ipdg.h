@@ -65,6 +65,7 @@ typedef struct {
   double bnorm;        /* ||b||_2 (global over ranks) */
   int32_t status;      /* IPDG_OK, IPDG_NOT_CONVERGED or IPDG_EBREAKDOWN */
   int32_t reserved;
+  double seconds;      /* host wall time of the solve call (ipdg_pcg_solve*, ipdg_loopback_pcg_solve) */
 } ipdg_stats;
 
 /* Create a context for degree N on CUDA device `device`.  Builds the reference
@@ -86,7 +87,9 @@ int ipdg_upload_mesh(ipdg_ctx ctx, int64_t K, int64_t Nv, const double* VX, cons
 /* Au = A u (device pointers, K*Np float64 each; in-place not allowed).  lambda >= 0. */
 int ipdg_ax(ipdg_ctx ctx, const double* u, double* Au, double lambda, void* stream);
 
-/* d = diag(A) (device, K*Np), computed exactly from the reference operators. */
+/* d = diag(A) (device, K*Np), computed exactly from the reference operators: the point-Jacobi
+ * preconditioner D^{-1} of the BASELINE C4 "Jacobi-PCG" (P:219 PCG; reading R11 -- the paper's
+ * own velocity preconditioner is block Jacobi).  Same face/penalty terms as ipdg_ax. */
 int ipdg_diag(ipdg_ctx ctx, double* d, double lambda, void* stream);
 
 /* Mu = J^e M u per element (block-diagonal mass, Eq. elementOps). */
@@ -135,6 +138,10 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx ctx, int64_t n, double* ms_pass_a, double
 /* Host-buffer convenience (the e2e path): copies b (host) in, solves, copies x out. */
 int ipdg_pcg_solve_host(ipdg_ctx ctx, const double* b_host, double* x_host, double lambda, int precond,
                         double tol, int64_t maxit, ipdg_stats* stats, void* stream);
+
+/* Every blocking call of the multi-GPU path waits by polling (cudaEventQuery) and checks
+ * ncclCommGetAsyncError on each poll: a failed or hung peer aborts the communicator and returns
+ * IPDG_ENCCL instead of blocking forever.  Timeout: environment IPDG_WAIT_TIMEOUT_S (default 600 s). */
 
 /* ---- multi-GPU (one process per GPU; NCCL over NVLink) ----
  * ipdg_comm_init: nccl_unique_id points to the 128-byte ncclUniqueId broadcast by the caller

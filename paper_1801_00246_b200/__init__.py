@@ -186,7 +186,7 @@ class Ipdg:
         rc = lib().ipdg_pcg_solve(self.ctx, _ptr(b), _ptr(x), float(lam), int(precond), float(tol), int(maxit),
                                   ctypes.byref(st), _stream(stream))
         check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
-        return x, dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+        return x, dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status, seconds=st.seconds)
 
     def pcg_begin(self, b, x, lam=0.0, precond=1, tol=1e-8, stream=None):
         self._workspace()
@@ -207,7 +207,7 @@ class Ipdg:
         st = ipdg_stats()
         rc = lib().ipdg_pcg_end(self.ctx, ctypes.byref(st), _stream(stream))
         check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
-        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status, seconds=st.seconds)
 
     def pcg_solve_host(self, b_host, x_host, lam=0.0, precond=1, tol=1e-8, maxit=10000, stream=None):
         """e2e path: host (pinned) numpy/torch CPU buffers in and out."""
@@ -217,7 +217,7 @@ class Ipdg:
                                        float(lam), int(precond), float(tol), int(maxit), ctypes.byref(st),
                                        _stream(stream))
         check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
-        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status)
+        return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status, seconds=st.seconds)
 
     # ---- introspection
     def refop(self, name):
@@ -279,7 +279,7 @@ def loopback_pcg_solve(ops, bs, xs, lam=0.0, precond=1, tol=1e-8, maxit=10000, s
     rc = lib().ipdg_loopback_pcg_solve(ctxs, P, bp, xp, float(lam), int(precond), float(tol), int(maxit), st,
                                        _stream(stream))
     check(rc, ops[0].ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
-    return [dict(iterations=s.iterations, rel_residual=s.rel_residual, bnorm=s.bnorm, status=s.status) for s in st]
+    return [dict(iterations=s.iterations, rel_residual=s.rel_residual, bnorm=s.bnorm, status=s.status, seconds=s.seconds) for s in st]
 
 
 def nccl_unique_id():

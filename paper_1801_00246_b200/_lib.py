@@ -27,7 +27,7 @@ OPS = dict(r=0, s=1, Dr=2, Ds=3, M=4, M1D=5, LIFT=6, Fmask=7)
 
 class ipdg_stats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("rel_residual", ctypes.c_double), ("bnorm", ctypes.c_double),
-                ("status", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("status", ctypes.c_int32), ("reserved", ctypes.c_int32), ("seconds", ctypes.c_double)]
 
 
 _c = ctypes

@@ -18,6 +18,10 @@
 //             r -= alpha_k Ap; red_B = (r.z, r.r); it = k               [+ allreduce(2)]
 //   end:    pending x += alpha_k p_k if no stop was decided; stats to host.
 #include "ctx.h"
+
+#include <chrono>
+#include <cstdlib>
+#include <thread>
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
 #include "sipdg_pipe.cuh"
@@ -978,6 +982,51 @@ int ipdg_pcg_iterate_profiled(ipdg_ctx c, int64_t n, double* ms_a, double* ms_b,
   return IPDG_OK;
 }
 
+// Wait for `s` by polling: with a communicator, every poll also checks ncclCommGetAsyncError, and a
+// failure or the timeout (IPDG_WAIT_TIMEOUT_S, default 600 s) aborts the communicator and fails with
+// IPDG_ENCCL instead of blocking forever on a dead peer (failure detection).
+static int wait_stream(ipdg_ctx c, cudaStream_t s) {
+  if (!c->comm) {
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return IPDG_OK;
+  }
+  static const double timeout = [] {
+    const char* e = std::getenv("IPDG_WAIT_TIMEOUT_S");
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0.0 ? v : 600.0;
+  }();
+  cudaEvent_t ev;
+  CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventRecord(ev, s));
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = IPDG_OK;
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      c->err = std::string("wait: ") + cudaGetErrorString(q);
+      rc = IPDG_ECUDA;
+      break;
+    }
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &ar) != ncclSuccess || ar != ncclSuccess) {
+      c->err = std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar);
+      rc = IPDG_ENCCL;
+    } else if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout) {
+      c->err = "NCCL wait timed out (IPDG_WAIT_TIMEOUT_S)";
+      rc = IPDG_ENCCL;
+    }
+    if (rc != IPDG_OK) {
+      ncclCommAbort(c->comm);  // unblocks the stream's NCCL kernels
+      c->comm = nullptr;
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  cudaEventDestroy(ev);
+  return rc;
+}
+
 int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
   if (!c) return IPDG_EINVAL;
   if (!c->x) FAIL(c, IPDG_ESTATE, "ipdg_pcg_end before ipdg_pcg_begin");
@@ -991,7 +1040,7 @@ int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
   CUDA_TRY(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(c, cudaStreamSynchronize(s));
+  TRY(wait_stream(c, s));
   const PcgState& h = *c->st_host;
   if (stats) {
     stats->iterations = h.stop_iter;
@@ -999,6 +1048,7 @@ int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
     stats->rel_residual = h.bb > 0 ? std::sqrt(h.final_rr / h.bb) : 0.0;
     stats->status = h.status;
     stats->reserved = 0;
+    stats->seconds = 0.0;
   }
   if (h.status == -4) FAIL(c, IPDG_EBREAKDOWN, "PCG breakdown at iteration %lld", (long long)h.stop_iter);
   return h.status == 1 ? IPDG_NOT_CONVERGED : IPDG_OK;
@@ -1007,6 +1057,7 @@ int ipdg_pcg_end(ipdg_ctx c, ipdg_stats* stats, void* stream) {
 int ipdg_pcg_solve(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, int64_t maxit,
                    ipdg_stats* stats, void* stream) {
   if (!c || maxit < 0) return IPDG_EINVAL;
+  const auto t_start = std::chrono::steady_clock::now();
   cudaStream_t s = (cudaStream_t)stream;
   TRY(ipdg_pcg_begin(c, b, x, lambda, precond, tol, stream));
   TRY(set_maxit(c, maxit, s));
@@ -1018,16 +1069,19 @@ int ipdg_pcg_solve(ipdg_ctx c, const double* b, double* x, double lambda, int pr
     TRY(ipdg_pcg_iterate(c, n, stream));
     done += n;
     CUDA_TRY(c, cudaMemcpyAsync(&c->st_host->stop_iter, &c->st->stop_iter, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(c, cudaStreamSynchronize(s));
+    TRY(wait_stream(c, s));
     if (c->st_host->stop_iter >= 0) break;
     chunk = std::min<int64_t>(chunk * 2, 8 * kChunk);
   }
-  return ipdg_pcg_end(c, stats, stream);
+  const int rc = ipdg_pcg_end(c, stats, stream);
+  if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  return rc;
 }
 
 int ipdg_pcg_solve_host(ipdg_ctx c, const double* b_host, double* x_host, double lambda, int precond, double tol,
                         int64_t maxit, ipdg_stats* stats, void* stream) {
   if (!c || !b_host || !x_host) return IPDG_EINVAL;
+  const auto t_start = std::chrono::steady_clock::now();
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
   cudaStream_t s = (cudaStream_t)stream;
   TRY(ensure_ws(c));
@@ -1050,7 +1104,8 @@ int ipdg_pcg_solve_host(ipdg_ctx c, const double* b_host, double* x_host, double
   const int rc = ipdg_pcg_solve(c, bd, xd, lambda, precond, tol, maxit, stats, stream);
   if (rc < 0) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(x_host, xd, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(c, cudaStreamSynchronize(s));
+  TRY(wait_stream(c, s));
+  if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return rc;
 }
 
@@ -1094,6 +1149,7 @@ static int loop_exchange(ipdg_ctx* cs, int P, cudaStream_t s) {
 int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double* const* x, double lambda, int precond,
                             double tol, int64_t maxit, ipdg_stats* stats, void* stream) {
   if (!cs || P < 1 || !b || !x || maxit < 0) return IPDG_EINVAL;
+  const auto t_start = std::chrono::steady_clock::now();
   for (int p = 0; p < P; ++p)
     if (!cs[p] || cs[p]->N != cs[0]->N || cs[p]->device != cs[0]->device || !b[p] || !x[p]) return IPDG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1166,6 +1222,8 @@ int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double*
   };
   const int rc = run();
   cudaFree(dsts);
+  if (stats)
+    for (int p = 0; p < P; ++p) stats[p].seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return rc;
 }
 

@@ -191,3 +191,21 @@ def test_c4_recipe_small_cylinder():
     true_o = np.linalg.norm(b.ravel() - A @ xo) / np.linalg.norm(b)
     r = b.ravel() - A @ x.cpu().numpy().ravel()
     assert np.linalg.norm(r) <= max(1e-8, true_o) * np.linalg.norm(b) * (1 + 1e-6)
+
+
+def test_single_rank_nccl_communicator_solve():
+    """With a (one-rank) NCCL communicator every blocking wait polls ncclCommGetAsyncError (failure
+    detection); the solve must be unchanged and report its wall time."""
+    from paper_1801_00246_b200 import nccl_unique_id
+    m = meshgen.square(8, jitter=0.2, diag="random", order="morton", seed=5)
+    N = 3
+    ref = RefElem(N)
+    A = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], ref)
+    b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], ref, meshgen.sin_sin_forcing)
+    op = Ipdg(N)
+    op.comm_init(nccl_unique_id(), 1, 0)
+    op.upload_mesh(m)
+    x, st = op.pcg_solve(gpu(b), precond=1, tol=1e-9, maxit=5000)
+    _, sto = solvers.pcg(lambda v: A @ v, b.ravel(), 1e-9, 5000, dinv=1.0 / A.diagonal())
+    assert abs(st["iterations"] - sto["iterations"]) <= 1
+    assert st["seconds"] > 0.0

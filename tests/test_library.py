@@ -60,3 +60,31 @@ def test_host_refops_match_oracle(N):
     assert np.abs(get("M1D", Nfp * Nfp).reshape(Nfp, Nfp) - ref.M1D).max() < 1e-14
     assert np.abs(get("LIFT", Np * 3 * Nfp).reshape(Np, 3 * Nfp) - ref.LIFT).max() < 1e-11 * np.abs(ref.LIFT).max()
     assert np.array_equal(get("Fmask", 3 * Nfp).reshape(3, Nfp).astype(int), ref.Fmask)
+
+
+def test_stats_struct_matches_header():
+    """ipdg_stats as declared in include/ipdg.h: int64, 2 doubles, 2 int32, double = 40 bytes."""
+    import ctypes
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ipdg.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} ipdg_stats;", hdr, re.S).group(1)
+    fields = re.findall(r"^\s*(int64_t|double|int32_t)\s+(\w+);", body, re.M)
+    assert [n for _, n in fields] == [n for n, _ in _lib.ipdg_stats._fields_]
+    assert ctypes.sizeof(_lib.ipdg_stats) == 40
+
+
+def test_tangential_face_derivative_identity():
+    """The k_tpb face-derivative split (sipdg_tpb.cuh) rests on: the derivative of u ALONG face f at its
+    nodes depends only on the face values (the nodal basis functions of the other nodes vanish on the
+    face, so their tangential derivative there is zero), via one 1-D matrix D1D for all three faces
+    (face 0: d/dr, face 1: d/ds - d/dr, face 2: d/ds, face nodes in ascending order).  Checked on the
+    oracle's reference element for every degree."""
+    for N in range(1, 9):
+        ref = RefElem(N)
+        F = ref.Fmask
+        D1D = ref.Dr[np.ix_(F[0], F[0])]
+        for f, T in ((0, ref.Dr), (1, ref.Ds - ref.Dr), (2, ref.Ds)):
+            rows = T[F[f]]
+            want = np.zeros_like(rows)
+            want[:, F[f]] = D1D
+            assert np.abs(rows - want).max() <= 1e-10 * np.abs(ref.Dr).max(), (N, f)
