@@ -219,6 +219,20 @@ class Ipdg:
         check(rc, self.ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
         return dict(iterations=st.iterations, rel_residual=st.rel_residual, bnorm=st.bnorm, status=st.status, seconds=st.seconds)
 
+    def pmg_apply(self, r, out=None, lam=0.0, stream=None):
+        """One p-multigrid V-cycle z = B r (the IPDG_PRECOND_PMG preconditioner)."""
+        self._workspace()
+        z = torch_empty_like(r) if out is None else out
+        check(lib().ipdg_pmg_apply(self.ctx, _ptr(r), _ptr(z), float(lam), _stream(stream)), self.ctx)
+        return z
+
+    def pmg_info(self):
+        deg = (ctypes.c_int * 16)()
+        lm = (ctypes.c_double * 16)()
+        n = lib().ipdg_pmg_info(self.ctx, deg, lm, 16)
+        check(min(n, 0), self.ctx)
+        return [(deg[i], lm[i]) for i in range(n)]
+
     # ---- introspection
     def refop(self, name):
         n = {"r": self.Np, "s": self.Np, "Dr": self.Np ** 2, "Ds": self.Np ** 2, "M": self.Np ** 2,
@@ -280,6 +294,11 @@ def loopback_pcg_solve(ops, bs, xs, lam=0.0, precond=1, tol=1e-8, maxit=10000, s
                                        _stream(stream))
     check(rc, ops[0].ctx, ok=(_lib.IPDG_OK, _lib.IPDG_NOT_CONVERGED))
     return [dict(iterations=s.iterations, rel_residual=s.rel_residual, bnorm=s.bnorm, status=s.status, seconds=s.seconds) for s in st]
+
+
+def torch_empty_like(t):
+    import torch
+    return torch.empty_like(t)
 
 
 def nccl_unique_id():

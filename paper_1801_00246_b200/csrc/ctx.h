@@ -55,6 +55,21 @@ struct ipdg_ctx_s {
   int nbt_split[2] = {0, 0};
   size_t smem_tpb_m[2] = {0, 0};  // [mode]
   bool tpb_ok[2][2] = {{false, false}, {false, false}};  // [mode][lam] fits on an SM
+  // p-multigrid preconditioner (IPDG_PRECOND_PMG; pmg.cuh, R22-R25): level 0 is this context,
+  // levels 1.. are child contexts of degree d_l on the same mesh
+  struct PmgLevel {
+    ipdg_ctx ctx = nullptr;   // child context (level 0: null, the parent)
+    int N = 0, Np = 0;
+    double lmax = 0.0;
+    double* buf = nullptr;    // dinv | b | x | r | d | t | y, K*Np each (256-byte aligned)
+    int64_t seg = 0;          // doubles per vector
+    double* I = nullptr;      // prolongation from level l+1 (Np x Np_{l+1}, row-major), device
+  };
+  std::vector<PmgLevel> pmg;
+  double pmg_lambda = -1.0;
+  PcgState* pmg_gate = nullptr;   // PCG state that gates the cycle's vector kernels (null: ipdg_pmg_apply)
+  std::vector<int32_t> pend_etov;  // mesh kept for the child contexts
+  double tau_scale = 1.0;
   int grid_cap = 0;  // debug: cap on every persistent grid (0 = off)
   int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4), 4 pipelined fused
   // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit

@@ -25,6 +25,7 @@
 #include "sipdg_kernels.cuh"
 #include "sipdg_split.cuh"
 #include "sipdg_pipe.cuh"
+#include "pmg.cuh"
 
 #include <numeric>
 
@@ -81,8 +82,19 @@ static int ghost_cap(int N, int device) {
 static void free_ws(ipdg_ctx c);
 
 // drops every mesh-sized buffer, including the PCG workspace binding (its layout depends on K + H)
+static void free_pmg(ipdg_ctx c) {
+  for (auto& L : c->pmg) {
+    if (L.ctx) ipdg_destroy(L.ctx);
+    if (L.buf) cudaFree(L.buf);
+    if (L.I) cudaFree(L.I);
+  }
+  c->pmg.clear();
+  c->pmg_lambda = -1.0;
+}
+
 static void free_mesh(ipdg_ctx c) {
   free_ws(c);
+  free_pmg(c);
   if (c->hostio) cudaFree(c->hostio);
   c->hostio = nullptr;
   c->hostio_n = 0;
@@ -271,6 +283,8 @@ int ipdg_upload_mesh(ipdg_ctx c, int64_t K, int64_t Nv, const double* VX, const 
     }
   c->pend_VX.assign(VX, VX + Nv);
   c->pend_VY.assign(VY, VY + Nv);
+  c->pend_etov.assign(EToV, EToV + K * 3);
+  c->tau_scale = tau_scale;
   c->tau_c = 0.5 * (c->N + 1) * (c->N + 2) * tau_scale;
   c->pend_remote = nremote;
   if (nremote > 0) return IPDG_OK;  // completed by ipdg_upload_halo
@@ -792,12 +806,14 @@ static int halo_for_p(ipdg_ctx c, cudaStream_t s) {
   return halo_exchange(c, s);
 }
 
+static int pmg_apply(ipdg_ctx c, cudaStream_t s);
 static int pass_b(ipdg_ctx c, cudaStream_t s) {
   if (c->precond == IPDG_PRECOND_BLOCK_JACOBI) DISPATCH(c->N, pass_b_bj(c, false, nullptr, s));
-  k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond ? c->dinv : nullptr, c->zb,
-                                        c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
+  k_pcg_b<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, c->r, c->Ap, c->precond == IPDG_PRECOND_JACOBI ? c->dinv : nullptr,
+                                        c->zb, c->st, c->partials, c->counter, c->xb ? c->x : nullptr, c->pe, c->po);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
+  if (c->precond == IPDG_PRECOND_PMG) TRY(pmg_apply(c, s));
   return IPDG_OK;
 }
 
@@ -851,11 +867,155 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
   return IPDG_OK;
 }
 
+// ---- p-multigrid preconditioner (IPDG_PRECOND_PMG; pmg.cuh, oracle/pmg.py, R22-R25)
+static int level_ax(ipdg_ctx c, int l, const double* u, double* Au, cudaStream_t s) {
+  ipdg_ctx lc = l == 0 ? c : c->pmg[l].ctx;
+  DISPATCH(lc->N, ax(lc, u, Au, c->pmg_lambda, s));
+}
+
+static double* lvec(ipdg_ctx c, int l, int which) {  // 0 dinv, 1 b, 2 x, 3 r, 4 d, 5 t, 6 y
+  auto& L = c->pmg[l];
+  if (l == 0 && which == 0) return c->dinv;
+  return L.buf + which * L.seg;
+}
+
+// R24: two Chebyshev steps from x = 0 for A x = b at level l
+static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
+  auto& L = c->pmg[l];
+  const int64_t n = c->K * L.Np;
+  const double a = L.lmax / 10.0, cc = 1.1 * L.lmax;
+  const double theta = 0.5 * (cc + a), delta = 0.5 * (cc - a), sigma = theta / delta;
+  const double rho0 = 1.0 / sigma, rho1 = 1.0 / (2.0 * sigma - rho0);
+  double* d = lvec(c, l, 4);
+  double* t = lvec(c, l, 5);
+  const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  k_cheb0<<<g, 256, 0, s>>>(n, b, lvec(c, l, 0), 1.0 / theta, x, d, c->pmg_gate);
+  TRY(level_ax(c, l, x, t, s));
+  k_cheb1<<<g, 256, 0, s>>>(n, b, t, lvec(c, l, 0), rho1 * rho0, 2.0 * rho1 / delta, x, d, c->pmg_gate);
+  c->launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+// R25: x = V_l(b), zero initial guess
+static int vcycle(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
+  TRY(cheb(c, l, b, x, s));
+  if (l + 1 == (int)c->pmg.size()) return IPDG_OK;
+  auto& L = c->pmg[l];
+  auto& C = c->pmg[l + 1];
+  const int64_t n = c->K * L.Np, nc = c->K * C.Np;
+  const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  double* r = lvec(c, l, 3);
+  double* t = lvec(c, l, 5);
+  double* y = lvec(c, l, 6);
+  TRY(level_ax(c, l, x, t, s));
+  k_resid<<<g, 256, 0, s>>>(n, b, t, r, c->pmg_gate);
+  k_restrict<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(c->K, L.Np, C.Np, L.I, r, lvec(c, l + 1, 1), c->pmg_gate);
+  c->launches += 2;
+  TRY(vcycle(c, l + 1, lvec(c, l + 1, 1), lvec(c, l + 1, 2), s));
+  k_prolong<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, L.Np, C.Np, L.I, lvec(c, l + 1, 2), x, 1, c->pmg_gate);
+  TRY(level_ax(c, l, x, t, s));
+  k_resid<<<g, 256, 0, s>>>(n, b, t, r, c->pmg_gate);
+  c->launches += 2;
+  TRY(cheb(c, l, r, y, s));
+  k_axpy1<<<g, 256, 0, s>>>(n, y, x, c->pmg_gate);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+static int host_dot(ipdg_ctx c, int64_t n, const double* u, const double* v, double* dev, cudaStream_t s, double* out) {
+  k_dot<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(n, u, v, dev, nullptr, c->partials, c->counter);
+  c->launches++;
+  CUDA_TRY(c, cudaMemcpyAsync(out, dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  return IPDG_OK;
+}
+
+// R22-R24: levels d_0 = N > d_1 > ... > 1 (child contexts on the same mesh), Jacobi diagonals, lmax by
+// 20 power iterations, transfer matrices.  Level 0's diagonal is c->dinv (computed by pcg_setup).
+static int pmg_setup(ipdg_ctx c, double lambda, cudaStream_t s) {
+  if (!c->pmg.empty() && c->pmg_lambda == lambda) return IPDG_OK;
+  if (c->H > 0 || c->S > 0) FAIL(c, IPDG_ESTATE, "p-multigrid preconditioner: one partition only");
+  free_pmg(c);
+  c->pmg_lambda = lambda;
+  std::vector<int> deg{c->N};
+  while (deg.back() > 1) deg.push_back(std::max(1, deg.back() / 2));
+  const int64_t K = c->K, Nv = (int64_t)c->pend_VX.size();
+  for (size_t l = 0; l < deg.size(); ++l) {
+    ipdg_ctx_s::PmgLevel L;
+    L.N = deg[l];
+    L.Np = (L.N + 1) * (L.N + 2) / 2;
+    L.seg = (K * L.Np + 31) / 32 * 32;
+    if (l > 0) {
+      TRY(ipdg_create(&L.ctx, L.N, c->device));
+      c->pmg.push_back(L);  // owned from here on (free_pmg)
+      const int rc = ipdg_upload_mesh(L.ctx, K, Nv, c->pend_VX.data(), c->pend_VY.data(), c->pend_etov.data(),
+                                      c->pend_bc.data(), c->tau_scale);
+      if (rc != IPDG_OK) FAIL(c, rc, "p-multigrid level %d: %s", L.N, L.ctx->err.c_str());
+      L.ctx->variant = c->variant;
+    } else {
+      c->pmg.push_back(L);
+    }
+    auto& P = c->pmg.back();
+    CUDA_TRY(c, cudaMalloc(&P.buf, 7 * P.seg * sizeof(double)));
+    if (l > 0) {
+      TRY([&]() -> int { DISPATCH(P.N, diag(P.ctx, P.buf, lambda, s)); }());
+      k_recip<<<(unsigned)((K * P.Np + 255) / 256), 256, 0, s>>>(K * P.Np, P.buf);
+      c->launches++;
+    }
+  }
+  for (size_t l = 0; l + 1 < deg.size(); ++l) {
+    const RefOps& F = (l == 0) ? c->ref : c->pmg[l].ctx->ref;
+    const RefOps& Cr = c->pmg[l + 1].ctx->ref;
+    const std::vector<double> I = interp_matrix(F, Cr);
+    TRY(upload(c, &c->pmg[l].I, I.data(), I.size()));
+  }
+  // lmax of D^{-1} A per level (R24)
+  double* dev = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dev, sizeof(double)));
+  for (size_t l = 0; l < deg.size(); ++l) {
+    const int64_t n = K * c->pmg[l].Np;
+    double* v = lvec(c, (int)l, 1);
+    double* w = lvec(c, (int)l, 2);
+    double* t = lvec(c, (int)l, 5);
+    const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    k_pmg_start<<<g, 256, 0, s>>>(n, v);
+    double lam = 0.0;
+    for (int it = 0; it < 20; ++it) {
+      TRY(level_ax(c, (int)l, v, t, s));
+      k_scale<<<g, 256, 0, s>>>(n, lvec(c, (int)l, 0), t, w);
+      double ww = 0.0, vv = 0.0;
+      TRY(host_dot(c, n, w, w, dev, s, &ww));
+      TRY(host_dot(c, n, v, v, dev, s, &vv));
+      lam = std::sqrt(ww) / std::sqrt(vv);
+      TRY(host_dot(c, n, w, w, dev, s, &ww));  // leaves w.w in dev for the normalisation
+      k_normalize<<<g, 256, 0, s>>>(n, w, dev, v);
+      c->launches += 2;
+    }
+    c->pmg[l].lmax = lam;
+  }
+  cudaFree(dev);
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
+// z = V(r) and rho = r.z -> st->red_B[0] (after the Jacobi-free pass B / init wrote z = r and the norms)
+static int pmg_apply(ipdg_ctx c, cudaStream_t s) {
+  c->pmg_gate = c->st;
+  TRY(vcycle(c, 0, c->r, c->zb, s));
+  const int64_t n = c->K * c->ref.Np;
+  k_dot<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(n, c->r, c->zb, nullptr, c->st, c->partials, c->counter);
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return IPDG_OK;
+}
+
 // PCG setup shared by ipdg_pcg_begin and the loopback group solve: argument checks, workspace, Jacobi
 // diagonal, device state (no Ax, no iteration graphs)
 static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int precond, double tol, bool dir,
                      cudaStream_t s) {
-  if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || precond < 0 || precond > 2) return IPDG_EINVAL;
+  if (!c || !b || !x || !(lambda >= 0.0) || !(tol >= 0.0) || precond < 0 || precond > 3) return IPDG_EINVAL;
   if (precond == IPDG_PRECOND_BLOCK_JACOBI && !(lambda > 0.0))
     FAIL(c, IPDG_EINVAL, "block-Jacobi (scaled inverse mass) preconditioning needs lambda > 0");
   if (c->K == 0) FAIL(c, IPDG_ESTATE, "pcg before ipdg_upload_mesh");
@@ -866,13 +1026,14 @@ static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int 
   if (precond == IPDG_PRECOND_BLOCK_JACOBI && !c->Minv) {
     TRY(upload(c, &c->Minv, c->ref.Minv.data(), c->ref.Minv.size()));
   }
-  if (precond == IPDG_PRECOND_JACOBI && !(c->dinv_valid && c->dinv_lambda == lambda)) {
+  if ((precond == IPDG_PRECOND_JACOBI || precond == IPDG_PRECOND_PMG) && !(c->dinv_valid && c->dinv_lambda == lambda)) {
     TRY([&]() -> int { DISPATCH(c->N, diag(c, c->dinv, lambda, s)); }());
     k_recip<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, c->dinv);
     c->launches++;
     c->dinv_valid = true;
     c->dinv_lambda = lambda;
   }
+  if (precond == IPDG_PRECOND_PMG) TRY(pmg_setup(c, lambda, s));
   c->x = x;
   c->lambda = lambda;
   c->precond = precond;
@@ -891,10 +1052,11 @@ static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int 
 // r = b - A x (A x already in c->Ap), z, partial (r.z, r.r, b.b) -> st->red_B (before the all-reduce)
 static int pcg_init_residual(ipdg_ctx c, const double* b, cudaStream_t s) {
   if (c->precond == IPDG_PRECOND_BLOCK_JACOBI) DISPATCH(c->N, pass_b_bj(c, true, b, s));
-  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, b, c->Ap, c->r, c->precond ? c->dinv : nullptr, c->zb, c->st,
-                                         c->partials, c->counter);
+  k_pcg_init<<<vec_grid(c), 256, 0, s>>>(c->K * c->ref.Np, b, c->Ap, c->r, c->precond == IPDG_PRECOND_JACOBI ? c->dinv : nullptr,
+                                         c->zb, c->st, c->partials, c->counter);
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
+  if (c->precond == IPDG_PRECOND_PMG) TRY(pmg_apply(c, s));
   return IPDG_OK;
 }
 
@@ -1062,7 +1224,7 @@ int ipdg_pcg_solve(ipdg_ctx c, const double* b, double* x, double lambda, int pr
   TRY(ipdg_pcg_begin(c, b, x, lambda, precond, tol, stream));
   TRY(set_maxit(c, maxit, s));
   int64_t done = 0;
-  int64_t chunk = kChunk;
+  int64_t chunk = (precond == IPDG_PRECOND_PMG) ? 4 : kChunk;
   while (true) {
     const int64_t n = std::min<int64_t>(chunk, maxit + 1 - done);
     if (n <= 0) break;
@@ -1071,7 +1233,8 @@ int ipdg_pcg_solve(ipdg_ctx c, const double* b, double* x, double lambda, int pr
     CUDA_TRY(c, cudaMemcpyAsync(&c->st_host->stop_iter, &c->st->stop_iter, sizeof(long long), cudaMemcpyDeviceToHost, s));
     TRY(wait_stream(c, s));
     if (c->st_host->stop_iter >= 0) break;
-    chunk = std::min<int64_t>(chunk * 2, 8 * kChunk);
+    // a p-multigrid iteration is ~10 Ax: short chunks (the level Ax kernels are not gated by the stop)
+    chunk = (precond == IPDG_PRECOND_PMG) ? 4 : std::min<int64_t>(chunk * 2, 8 * kChunk);
   }
   const int rc = ipdg_pcg_end(c, stats, stream);
   if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
@@ -1152,6 +1315,7 @@ int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double*
   const auto t_start = std::chrono::steady_clock::now();
   for (int p = 0; p < P; ++p)
     if (!cs[p] || cs[p]->N != cs[0]->N || cs[p]->device != cs[0]->device || !b[p] || !x[p]) return IPDG_EINVAL;
+  if (precond == IPDG_PRECOND_PMG) FAIL(cs[0], IPDG_ESTATE, "loopback PCG: p-multigrid needs one partition");
   cudaStream_t s = (cudaStream_t)stream;
   bool dir = false;
   for (int p = 0; p < P; ++p) dir |= cs[p]->has_dirichlet;
@@ -1225,6 +1389,35 @@ int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double*
   if (stats)
     for (int p = 0; p < P; ++p) stats[p].seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return rc;
+}
+
+int ipdg_pmg_apply(ipdg_ctx c, const double* r, double* z, double lambda, void* stream) {
+  if (!c || !r || !z || r == z || !(lambda >= 0.0)) return IPDG_EINVAL;
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_pmg_apply before ipdg_upload_mesh");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ensure_ws(c));
+  TRY(ensure_partials(c));
+  const int64_t n = c->K * c->ref.Np;
+  if (!(c->dinv_valid && c->dinv_lambda == lambda)) {
+    TRY([&]() -> int { DISPATCH(c->N, diag(c, c->dinv, lambda, s)); }());
+    k_recip<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, c->dinv);
+    c->launches++;
+    c->dinv_valid = true;
+    c->dinv_lambda = lambda;
+  }
+  TRY(pmg_setup(c, lambda, s));
+  c->pmg_gate = nullptr;
+  return vcycle(c, 0, r, z, s);
+}
+
+int ipdg_pmg_info(ipdg_ctx c, int* degrees, double* lmax, int cap) {
+  if (!c || cap < 0) return IPDG_EINVAL;
+  const int L = (int)c->pmg.size();
+  for (int l = 0; l < L && l < cap; ++l) {
+    if (degrees) degrees[l] = c->pmg[l].N;
+    if (lmax) lmax[l] = c->pmg[l].lmax;
+  }
+  return L;
 }
 
 int ipdg_comm_init(ipdg_ctx c, const void* id, int nranks, int rank) {

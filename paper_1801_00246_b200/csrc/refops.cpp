@@ -225,4 +225,20 @@ RefOps build_refops(int N) {
   return R;
 }
 
+std::vector<double> interp_matrix(const RefOps& F, const RefOps& Cr) {
+  const int nf = F.Np, nc = Cr.Np, N = Cr.N;
+  std::vector<double> Vc(nc * nc), Vfc(nf * nc);
+  for (int n = 0; n < nc; ++n) {
+    int k = 0;
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j, ++k) psi(i, j, Cr.r[n], Cr.s[n], &Vc[n * nc + k], nullptr, nullptr);
+  }
+  for (int n = 0; n < nf; ++n) {
+    int k = 0;
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j, ++k) psi(i, j, F.r[n], F.s[n], &Vfc[n * nc + k], nullptr, nullptr);
+  }
+  return matmul(Vfc, invert(Vc, nc), nf, nc, nc);
+}
+
 }  // namespace ipdg

@@ -18,5 +18,8 @@ struct RefOps {
 };
 
 RefOps build_refops(int N);
+// p-multigrid transfer (R23): (fine.Np x coarse.Np) values of the degree-coarse nodal basis at
+// the degree-fine nodes, V_c(r_f, s_f) V_c^{-1}
+std::vector<double> interp_matrix(const RefOps& fine, const RefOps& coarse);
 
 }  // namespace ipdg
