@@ -57,7 +57,7 @@ extern "C" {
 #define IPDG_PRECOND_BLOCK_JACOBI 2 /* screened Poisson (lambda > 0, else IPDG_EINVAL): the scaled inverse
                                      * mass matrix on each element, (lambda J^e M)^{-1} */
 #define IPDG_PRECOND_PMG 3 /* matrix-free p-multigrid V-cycle (P:223-225 pMG levels; DESIGN.md
-                              R22-R25): degrees N -> floor(N/2) -> ... -> 1 on the same mesh, nodal
+                              R22-R26): degrees N -> floor(N/2) -> ... -> 1 on the same mesh, nodal
                               interpolation / its transpose between them, degree-2 Chebyshev smoothing
                               of D^-1 A on [lmax/10, 1.1 lmax] (lmax by 20 power iterations); the degree-1
                               level is only smoothed (the paper's AMG tail is out of scope).  One
@@ -141,7 +141,7 @@ int ipdg_pcg_end(ipdg_ctx ctx, ipdg_stats* stats, void* stream);
  * direction update + Ax + p.Ap) and pass B (residual update + dots).  Synchronizes. */
 int ipdg_pcg_iterate_profiled(ipdg_ctx ctx, int64_t n, double* ms_pass_a, double* ms_pass_b, void* stream);
 
-/* One p-multigrid V-cycle z = B r (IPDG_PRECOND_PMG's preconditioner, R22-R25),
+/* One p-multigrid V-cycle z = B r (IPDG_PRECOND_PMG's preconditioner, R22-R26),
  * device vectors K x Np, builds the level hierarchy for `lambda` on first use (child contexts of
  * degrees N/2, ..., 1 on the same mesh, their diagonals and power-iteration lmax).  Async on `stream`
  * after the first (blocking) setup.  ipdg_pmg_info: number of levels (and, up to cap, their degrees

@@ -14,9 +14,11 @@ DESIGN.md reading:
   R24 smoother    degree-2 Chebyshev iteration on D_l^{-1} A_l (D_l = diag A_l) over [lmax/10, 1.1 lmax],
                   lmax from 20 power iterations x <- D^{-1} A x / ||.||  (ratio of norms) from the fixed
                   start vector v_i = ((7919 i) mod 1009) / 1009 - 1/2 (i = global DOF index).
-                  The coarsest level (degree 1) applies the same smoother once (no AMG tail).
+  R26 coarse      the AMG tail is out of scope, so the degree-1 level is solved approximately by a
+                  longer Chebyshev polynomial: 16 steps over [1.1 lmax / 250, 1.1 lmax] (a fixed linear
+                  symmetric operator, positive on the spectrum); with N = 1 it is the whole cycle.
   R25 cycle       one V-cycle with zero initial guess: x = S_l b; x += P_l V_{l+1}(R_l (b - A_l x));
-                  x += S_l (b - A_l x); at level L: x = S_L b.  S_l (the zero-start smoother) is a
+                  x += S_l (b - A_l x); at level L: x = C_L b (R26).  S_l (the zero-start smoother) is a
                   polynomial in D^{-1}A times D^{-1}: symmetric, so the cycle is a fixed symmetric linear
                   operator, as CG requires.
 
@@ -27,6 +29,10 @@ import numpy as np
 
 from .assemble import assemble
 from .refelem import RefElem, vandermonde_2d
+
+
+# R26: the degree-1 level (no AMG tail) gets a longer Chebyshev polynomial over a wider interval
+COARSE_STEPS, COARSE_RATIO = 16, 250.0
 
 
 def schedule(N):
@@ -72,21 +78,26 @@ def power_lmax(A, dinv, iters=20):
     return lam
 
 
-def chebyshev(A, dinv, b, lmax):
-    """R24: two steps of the Chebyshev iteration for D^{-1} A x = D^{-1} b from x = 0 on [a, c] = [lmax/10, 1.1 lmax]
-    (textbook three-term form: theta = (c+a)/2, delta = (c-a)/2, sigma = theta/delta,
-    rho_0 = 1/sigma, d_0 = D^{-1} r_0 / theta, rho_1 = 1/(2 sigma - rho_0),
-    d_1 = rho_1 rho_0 d_0 + (2 rho_1/delta) D^{-1} r_1)."""
-    a, c = lmax / 10.0, 1.1 * lmax
+def chebyshev(A, dinv, b, lmax, steps=2, a=None):
+    """R24: `steps` steps of the Chebyshev iteration for D^{-1} A x = D^{-1} b from x = 0 on [a, c],
+    c = 1.1 lmax, a = lmax/10 (smoother; R26: the coarse level passes its own a and steps).  Textbook
+    three-term form: theta = (c+a)/2, delta = (c-a)/2, sigma = theta/delta, rho_0 = 1/sigma,
+    d_0 = D^{-1} r_0 / theta, then for m >= 1: rho_m = 1/(2 sigma - rho_{m-1}),
+    d_m = rho_m rho_{m-1} d_{m-1} + (2 rho_m/delta) D^{-1} r_m, with x_{m+1} = x_m + d_m, r_m = b - A x_m."""
+    c = 1.1 * lmax
+    a = lmax / 10.0 if a is None else a
     theta, delta = 0.5 * (c + a), 0.5 * (c - a)
     sigma = theta / delta
-    rho0 = 1.0 / sigma
+    rho = 1.0 / sigma
     d = dinv * b / theta          # zero start: r_0 = b
     x = d
-    rho1 = 1.0 / (2.0 * sigma - rho0)
-    r = b - A @ x
-    d = rho1 * rho0 * d + (2.0 * rho1 / delta) * (dinv * r)
-    return x + d
+    for _ in range(steps - 1):
+        rho_new = 1.0 / (2.0 * sigma - rho)
+        r = b - A @ x
+        d = rho_new * rho * d + (2.0 * rho_new / delta) * (dinv * r)
+        x = x + d
+        rho = rho_new
+    return x
 
 
 class PMG:
@@ -104,9 +115,9 @@ class PMG:
     def vcycle(self, b, l=0):
         """R25."""
         A, di, lm = self.A[l], self.dinv[l], self.lmax[l]
+        if l == len(self.degrees) - 1:  # R26: coarse level
+            return chebyshev(A, di, b, lm, steps=COARSE_STEPS, a=1.1 * lm / COARSE_RATIO)
         x = chebyshev(A, di, b, lm)
-        if l == len(self.degrees) - 1:
-            return x
         r = b - A @ x
         xc = self.vcycle(restrict(self.I[l], r), l + 1)
         x = x + prolong(self.I[l], xc)

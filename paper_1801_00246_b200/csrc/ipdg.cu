@@ -879,20 +879,28 @@ static double* lvec(ipdg_ctx c, int l, int which) {  // 0 dinv, 1 b, 2 x, 3 r, 4
   return L.buf + which * L.seg;
 }
 
-// R24: two Chebyshev steps from x = 0 for A x = b at level l
+// R24 / R26: `steps` Chebyshev steps from x = 0 for A x = b at level l over [a, 1.1 lmax] (smoother: 2 steps,
+// a = lmax / 10; coarsest level: kPmgCoarseSteps, a = 1.1 lmax / kPmgCoarseRatio)
 static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
   auto& L = c->pmg[l];
+  const bool coarse = (l + 1 == (int)c->pmg.size());
+  const int steps = coarse ? kPmgCoarseSteps : 2;
   const int64_t n = c->K * L.Np;
-  const double a = L.lmax / 10.0, cc = 1.1 * L.lmax;
+  const double cc = 1.1 * L.lmax, a = coarse ? cc / kPmgCoarseRatio : L.lmax / 10.0;
   const double theta = 0.5 * (cc + a), delta = 0.5 * (cc - a), sigma = theta / delta;
-  const double rho0 = 1.0 / sigma, rho1 = 1.0 / (2.0 * sigma - rho0);
   double* d = lvec(c, l, 4);
   double* t = lvec(c, l, 5);
   const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
   k_cheb0<<<g, 256, 0, s>>>(n, b, lvec(c, l, 0), 1.0 / theta, x, d, c->pmg_gate);
-  TRY(level_ax(c, l, x, t, s));
-  k_cheb1<<<g, 256, 0, s>>>(n, b, t, lvec(c, l, 0), rho1 * rho0, 2.0 * rho1 / delta, x, d, c->pmg_gate);
-  c->launches += 2;
+  c->launches++;
+  double rho = 1.0 / sigma;
+  for (int m = 1; m < steps; ++m) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    TRY(level_ax(c, l, x, t, s));
+    k_cheb1<<<g, 256, 0, s>>>(n, b, t, lvec(c, l, 0), rho_new * rho, 2.0 * rho_new / delta, x, d, c->pmg_gate);
+    c->launches++;
+    rho = rho_new;
+  }
   CUDA_TRY(c, cudaGetLastError());
   return IPDG_OK;
 }

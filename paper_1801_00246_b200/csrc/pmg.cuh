@@ -1,4 +1,4 @@
-// Matrix-free p-multigrid preconditioner kernels (R22-R25).
+// Matrix-free p-multigrid preconditioner kernels (R22-R26).
 // The level operators are the library's own SIPDG Ax at each degree (child contexts); these kernels are
 // the element-wise transfers, the Chebyshev smoother's vector steps and the reductions around them.
 // Every kernel takes the PCG state `gate` (or null) and does nothing once the solve has stopped, so the
@@ -9,6 +9,10 @@
 namespace ipdg {
 
 __device__ __forceinline__ bool gated(const PcgState* g) { return g && g->stop_iter >= 0; }
+
+// R26: the degree-1 level (no AMG tail) -- 16 Chebyshev steps over [1.1 lmax / 250, 1.1 lmax]
+constexpr int kPmgCoarseSteps = 16;
+constexpr double kPmgCoarseRatio = 250.0;
 
 // uf (+)= P uc element by element: uf[e][i] = sum_j I[i][j] uc[e][j]   (R23, I row-major npf x npc)
 static __global__ void k_prolong(int64_t K, int npf, int npc, const double* __restrict__ I, const double* __restrict__ uc,

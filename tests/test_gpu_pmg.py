@@ -1,5 +1,5 @@
 """GPU parity of the p-multigrid preconditioner (IPDG_PRECOND_PMG, DESIGN.md
-R22-R25) against oracle/pmg.py: the power-iteration lmax of every level, one V-cycle element by element,
+R22-R26) against oracle/pmg.py: the power-iteration lmax of every level, one V-cycle element by element,
 and PCG with the V-cycle as preconditioner (iterations within +-1 of the oracle's textbook PCG with the
 oracle's V-cycle; residual of the GPU solution)."""
 import functools

@@ -60,25 +60,35 @@ def test_restriction_is_the_transpose():
     assert abs(np.dot(pmg.prolong(I, uc), vf) - np.dot(uc, pmg.restrict(I, vf))) <= 1e-12
 
 
-def test_chebyshev_matches_the_residual_polynomial():
-    """Zero start, D = I, A = diag(lam): the error after the two steps is T_2((theta - lam)/delta) /
-    T_2(theta/delta) times the initial error, so x = (1 - q(lam)) / lam * b (closed form)."""
-    lam = np.linspace(0.05, 2.0, 40)
+def _cheb_T(k, t):
+    """Chebyshev polynomial of the first kind, closed form (cos / cosh)."""
+    t = np.asarray(t, dtype=np.float64)
+    out = np.empty_like(t)
+    m = np.abs(t) <= 1
+    out[m] = np.cos(k * np.arccos(t[m]))
+    out[t > 1] = np.cosh(k * np.arccosh(t[t > 1]))
+    out[t < -1] = (-1) ** k * np.cosh(k * np.arccosh(-t[t < -1]))
+    return out
+
+
+@pytest.mark.parametrize("steps,ratio", [(2, None), (5, 40.0), (16, 250.0)])
+def test_chebyshev_matches_the_residual_polynomial(steps, ratio):
+    """Zero start, D = I, A = diag(lam): the error after k steps is T_k((theta - lam)/delta) /
+    T_k(theta/delta) times the initial error, so x = (1 - q(lam)) / lam * b (closed form); k = 2 on
+    [lmax/10, 1.1 lmax] is the smoother (R24), k = 16 on [1.1 lmax/250, 1.1 lmax] the coarse level (R26)."""
+    lam = np.linspace(0.002, 2.0, 60)
     A = sp.diags(lam).tocsr()
     b = np.random.default_rng(2).standard_normal(lam.size)
     lmax = 2.0
-    a, c = lmax / 10.0, 1.1 * lmax
+    c = 1.1 * lmax
+    a = lmax / 10.0 if ratio is None else c / ratio
     theta, delta = 0.5 * (c + a), 0.5 * (c - a)
-
-    def T2(t):
-        return 2.0 * t * t - 1.0
-
-    q = T2((theta - lam) / delta) / T2(theta / delta)
-    x = pmg.chebyshev(A, np.ones_like(lam), b, lmax)
-    assert np.abs(x - (1.0 - q) / lam * b).max() <= 1e-13 * np.abs(b / lam).max()
-    # inside the interval the error is damped by at least 1/T_2(theta/delta)
+    q = _cheb_T(steps, (theta - lam) / delta) / _cheb_T(steps, np.array([theta / delta]))[0]
+    x = pmg.chebyshev(A, np.ones_like(lam), b, lmax, steps=steps, a=None if ratio is None else a)
+    assert np.abs(x - (1.0 - q) / lam * b).max() <= 1e-11 * np.abs(b / lam).max()
+    # inside the interval the error is damped by at least 1/T_k(theta/delta)
     inside = (lam >= a) & (lam <= c)
-    assert np.abs(q[inside]).max() <= 1.0 / T2(theta / delta) + 1e-15
+    assert np.abs(q[inside]).max() <= 1.0 / _cheb_T(steps, np.array([theta / delta]))[0] + 1e-14
 
 
 def _small(N, nx=5):
@@ -131,3 +141,16 @@ def test_level_operators_are_the_rediscretised_sipdg_operators():
     for d, A in zip(H.degrees, H.A):
         B = assemble(m["VX"], m["VY"], m["EToV"], m["bc"], RefElem(d))
         assert abs(A - B).max() == 0.0
+
+
+def test_iterations_grow_at_most_2x_under_refinement():
+    """S:504 / S:715 (the paper's VortexPreconditioner trend): PCG + p-multigrid iteration counts grow by at
+    most 2x across one uniform refinement at N = 3."""
+    its = []
+    for nx in (6, 12):
+        m, H = _small(3, nx=nx)
+        A = H.A[0]
+        b = solvers.rhs_mass_interp(m["VX"], m["VY"], m["EToV"], H.refs[0], meshgen.sin_sin_forcing).ravel()
+        _, st = solvers.pcg(lambda v: A @ v, b, 1e-8, 5000, apply_P=H.apply)
+        its.append(st["iterations"])
+    assert its[1] <= 2 * its[0], its
