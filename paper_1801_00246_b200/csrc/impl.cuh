@@ -386,12 +386,13 @@ struct Impl {
   // k_pipe moves whole rows with TMA bulk copies: operand vectors must be 16-byte aligned
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
   // Kernel actually used (1 fused k_sipdg, 2 split, 4 pipelined k_pipe, 5 gather, 6 thread-per-element
-  // block k_tpb).  Auto (variant 0), the fastest measured per degree on C3 (profiles/r02_c3_variants.jsonl):
-  // k_tpb for N <= 3 (Ax and PCG pass A), pipelined fused for N = 4, 5, split for N >= 6.
+  // block k_tpb).  Auto (variant 0), the fastest measured per degree (profiles/r02_variants_tpb_vs_pipe.jsonl,
+  // C3 and C2): k_tpb for N <= 5 (Ax and PCG pass A; C2 pass A at N = 4 ties with k_pipe, 78 vs 77 us),
+  // split for N >= 6 (k_tpb's register-resident rows spill there).
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : (N <= 3 ? 6 : 4);
+    if (k == 0) k = (N >= 6) ? 2 : 6;
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
     if (k == 6 && !(c->tpb_ok[mode][lam] && (!lam || TrB<N>::HAS_LAM) && (v == nullptr || aligned16(v)))) k = 1;
@@ -575,7 +576,7 @@ struct Impl {
     const bool lam = c->lambda != 0.0;
     if (k == 5) return launch_gather<MODE_PCG_A>(c, a, lam, s);
     if (k == 6) {
-      a.defer_x = 1;
+      a.defer_x = c->xb ? 0 : 1;
       if (c->split_a) {  // interior blocks, (wait for the halo exchange), halo-boundary blocks
         const int ni = c->nbt_split[0], nbd = c->nbt_split[1];
         a.red_part = (ni > 0 && nbd > 0) ? 1 : 0;

@@ -1045,7 +1045,13 @@ static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int 
   c->x = x;
   c->lambda = lambda;
   c->precond = precond;
-  c->xb = impl_ops(c->N)->resolve(c, 1, lambda != 0.0, x) == 4 && c->pipe_xb[lambda != 0.0];
+  {
+    const int kern = impl_ops(c->N)->resolve(c, 1, lambda != 0.0, x);
+#ifndef IPDG_TPB_XB
+#define IPDG_TPB_XB 0  // experiment: k_tpb leaves x += alpha p to pass B
+#endif
+    c->xb = (kern == 4 && c->pipe_xb[lambda != 0.0]) || (kern == 6 && IPDG_TPB_XB);
+  }
   PcgState h;
   std::memset(&h, 0, sizeof(h));
   h.tol2 = tol * tol;

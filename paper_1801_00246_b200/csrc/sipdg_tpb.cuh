@@ -85,15 +85,10 @@ struct TpbLayout {
   using T = TrB<N>;
   static constexpr int ROWS = 0;
   static constexpr int FT = ((T::E * T::NP + 1) + 1) & ~1;
-  // The face-record region first holds the staged p_{k-1} rows (PCG pass A) and the ghost-face rows
-  // (z, and p_{k-1} in PCG), all consumed before the face records are written.
-  __host__ __device__ static int gz(bool pcg) { return FT + (pcg ? T::E * T::NP : 0); }       // ghost rows
-  __host__ __device__ static int gp(int gmax, bool pcg) { return gz(pcg) + gmax * T::NP; }  // ghost p_{k-1}
-  __host__ __device__ static int ftn(int gmax, bool pcg) {
-    const int a = 2 * T::E * T::TS, b = gp(gmax, pcg) + (pcg ? gmax * T::NP : 0) - FT;
-    return ((a > b ? a : b) + 1) & ~1;
-  }
-  __host__ __device__ static int gft(int gmax, bool pcg) { return FT + ftn(gmax, pcg); }
+  // The face-record region first holds the staged p_{k-1} and x rows (PCG pass A), consumed by the
+  // formation pass before the face records are written (a block barrier in between).
+  static constexpr int FTN = (2 * T::E * T::TS > 2 * T::E * T::NP ? 2 * T::E * T::TS : 2 * T::E * T::NP);
+  __host__ __device__ static int gft(int, bool) { return FT + FTN; }
   __host__ __device__ static int mbar(int gmax, bool pcg) { return gft(gmax, pcg) + 2 * gmax * T::NFP; }
   __host__ __device__ static int total(int gmax, bool pcg) { return mbar(gmax, pcg) + 2; }
 };
@@ -237,90 +232,67 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  double* spo = sm + L::FT;                // PCG: p_{k-1} rows
-  double* gzs = sm + L::gz(PCG);           // ghost-face rows (z / u, or halo p_k)
-  double* gps = sm + L::gp(gmax, PCG);     // ghost-face rows of p_{k-1} (PCG)
+  double* spo = sm + L::FT;              // PCG: p_{k-1} rows
+  double* sx = sm + L::FT + E * NP;      // PCG: x rows
   if (bulk) {
     if (tid == 0) {
       const unsigned nb = (unsigned)nrow * 8u;
-      mbar_expect_tx(mbar, nb * (1u + (with_p ? 1u : 0u)));
+      mbar_expect_tx(mbar, nb * (1u + (with_p ? 1u : 0u) + (with_x ? 1u : 0u)));
       tma_load_1d(rows, U + g0, nb, mbar);
       if (with_p) tma_load_1d(spo, pold + g0, nb, mbar);
+      if (with_x) tma_load_1d(sx, a.x + g0, nb, mbar);
     }
   } else {
     for (int q = tid; q < nrow; q += NTHR) {
       rows[q] = U[g0 + q];
       if (with_p) spo[q] = pold[g0 + q];
+      if (with_x) sx[q] = a.x[g0 + q];
     }
   }
-  // x rows for the deferred update: coalesced loads into registers now, used by the formation pass
-  constexpr int XQ = (E * NP + NTHR - 1) / NTHR;
-  double xr[PCG ? XQ : 1];
-  if (with_x) {
-#pragma unroll
-    for (int i = 0; i < XQ; ++i) {
-      const int q = tid + i * NTHR;
-      xr[i] = q < nrow ? a.x[g0 + q] : 0.0;
-    }
-  }
-  // ghost faces: the neighbour rows stream into shared memory (cp.async) alongside the bulk copies
+
+  // ---- ghost faces, while the bulk copies are in flight: value and trace of the outside neighbour on
+  // the shared face, from its row in global memory (L2; PCG: p_k = z + beta p_{k-1}, the owner's FMA)
+  // into the ghost-face records (their own region: no ordering against the staging)
   const int gf0 = a.gfoff[b], Gb = a.gfoff[b + 1] - gf0;
 #ifndef IPDG_TPB_SKIP
 #define IPDG_TPB_SKIP 0  // debug: 1 = no ghost pass, 2 = no volume, 4 = no face phase (results wrong)
 #endif
-  for (int q = tid; q < Gb * NP; q += NTHR) {
-    const int g = q / NP, j = q - g * NP;
-    const int64_t n = a.gface[gf0 + g] >> 2;
-    if (n >= K) {
-      cp_async8(gzs + q, a.halo_p + (n - K) * NP + j);
-      if (with_p) gps[q] = 0.0;  // halo rows are p_k already
-    } else {
-      cp_async8(gzs + q, U + n * NP + j);
-      if (with_p) cp_async8(gps + q, pold + n * NP + j);
-    }
-  }
-  cp_async_commit();
-  int gent = 0;
-  double4 gn = make_double4(0.0, 0.0, 0.0, 0.0);
-  if (tid < Gb) {  // ghost-face owner thread: entry and chain-rule record
-    gent = a.gface[gf0 + tid];
-    gn = a.gG[gent >> 2];
-  }
-
-  if (bulk) mbar_wait(mbar, 0);
-  cp_async_wait_all();
-  __syncthreads();
-  // ---- ghost faces: value and trace of the outside neighbour on the shared face (rows from smem;
-  // PCG: p_k = z + beta p_{k-1}, the same FMA as the owner's)
   for (int g = tid; g < ((IPDG_TPB_SKIP & 1) ? 0 : Gb); g += NTHR) {
-    const int ent = (g == tid) ? gent : a.gface[gf0 + g];
+    const int ent = a.gface[gf0 + g];
+    const int64_t n = ent >> 2;
     const int fp = ent & 3;
-    const double4 gq = (g == tid) ? gn : a.gG[ent >> 2];
-    const bool halo = (ent >> 2) >= K;
     double un[NP];
+    if (n >= K) {
+      const double* h = a.halo_p + (n - K) * NP;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) un[j] = (with_p && !halo) ? fma(beta, gps[g * NP + j], gzs[g * NP + j]) : gzs[g * NP + j];
+      for (int j = 0; j < NP; ++j) un[j] = h[j];
+    } else {
+      const double* src = U + n * NP;
+      const double* po = pold + n * NP;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) un[j] = with_p ? fma(beta, po[j], src[j]) : src[j];
+    }
+    const double4 gq = a.gG[n];
     double2* go = gft + g * NFP;
     if (fp == 0) ghost_face<N, 0>(un, gq, go);
     else if (fp == 1) ghost_face<N, 1>(un, gq, go);
     else ghost_face<N, 2>(un, gq, go);
   }
 
+  if (bulk) mbar_wait(mbar, 0);
+  else __syncthreads();
   if (PCG) {  // p_k = z + beta p_{k-1} in place, p_k and the deferred x update x += alpha_{k-1} p_{k-1}
     const double alpha_prev = d.alpha_prev;
-#pragma unroll
-    for (int i = 0; i < XQ; ++i) {
-      const int q = tid + i * NTHR;
-      if (q < nrow) {
-        const double po = with_p ? spo[q] : 0.0;
-        const double v = with_p ? fma(beta, po, rows[q]) : rows[q];
-        rows[q] = v;
-        pnew[g0 + q] = v;
-        if (with_x) a.x[g0 + q] = fma(alpha_prev, po, xr[i]);
-      }
+#pragma unroll 4
+    for (int q = tid; q < nrow; q += NTHR) {
+      const double po = with_p ? spo[q] : 0.0;
+      const double v = with_p ? fma(beta, po, rows[q]) : rows[q];
+      rows[q] = v;
+      pnew[g0 + q] = v;
+      if (with_x) a.x[g0 + q] = fma(alpha_prev, po, sx[q]);
     }
   }
-  __syncthreads();  // p_k rows complete; ghost rows consumed before the face records overwrite them
+  __syncthreads();  // p_k rows complete; staging consumed before the face records overwrite it
 
   // ---- own elements (R per thread: slots tid + r NTHR): volume, own face values and traces.  Outer
   // products: NP independent accumulators per element, every constant feeds R FMAs.
