@@ -39,7 +39,7 @@ def peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-KERNEL_NAMES = {1: "k_sipdg", 2: "k_grad+k_flux", 4: "k_pipe", 5: "k_gather"}
+KERNEL_NAMES = {1: "k_sipdg", 2: "k_grad+k_flux", 4: "k_pipe", 5: "k_gather", 6: "k_tpb"}
 FP64_PEAK_TFLOPS = 36.8  # measured DFMA / DMMA peak on this pool's B200 (profiles/r01_micro_fp64.jsonl)
 
 

@@ -387,12 +387,13 @@ struct Impl {
   static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
   // Kernel actually used (1 fused k_sipdg, 2 split, 4 pipelined k_pipe, 5 gather, 6 thread-per-element
   // block k_tpb).  Auto (variant 0), the fastest measured per degree (profiles/r02_variants_tpb_vs_pipe.jsonl,
-  // C3 and C2): k_tpb for N <= 5 (Ax and PCG pass A; C2 pass A at N = 4 ties with k_pipe, 78 vs 77 us),
-  // split for N >= 6 (k_tpb's register-resident rows spill there).
+  // C3 and C2): k_tpb for N <= 5 (Ax and PCG pass A) except PCG pass A at N = 4, where k_pipe is 2 % faster
+  // on the bench mesh C2 (76.6 vs 78.1 us; C3: 320 vs 307 us), split for N >= 6 (k_tpb's register-resident
+  // rows spill there).
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : 6;
+    if (k == 0) k = (N >= 6) ? 2 : ((mode == 1 && N == 4) ? 4 : 6);
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
     if (k == 6 && !(c->tpb_ok[mode][lam] && (!lam || TrB<N>::HAS_LAM) && (v == nullptr || aligned16(v)))) k = 1;

@@ -18,5 +18,5 @@ timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/${TAG}_re
 timeout 900 python bench.py --sweep > $O/${TAG}_sweep.jsonl 2>&1; cut -c1-160 $O/${TAG}_sweep.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-solve --no-e2e > $O/${TAG}_launches.log 2>&1; tail -1 $O/${TAG}_launches.log
 # k_pipe launches of prof_run --ax 1 --pcg 6: Ax, Ax(x0) in pcg_begin, pass A of iterations 1..6 -> skip 4 = iteration 3
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_grad|k_flux|k_gather" -s 4 -c 1 -o $O/${TAG}_prof_passA python tools/prof_run.py --N 4 --ax 1 --pcg 6 > $O/${TAG}_prof_passA.log 2>&1; tail -1 $O/${TAG}_prof_passA.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_grad|k_flux|k_gather" -s 0 -c 1 -o $O/${TAG}_prof_ax python tools/prof_run.py --N 4 --ax 1 --pcg 0 > $O/${TAG}_prof_ax.log 2>&1; tail -1 $O/${TAG}_prof_ax.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_grad|k_flux|k_gather|k_tpb" -s 4 -c 1 -o $O/${TAG}_prof_passA python tools/prof_run.py --N 4 --ax 1 --pcg 6 > $O/${TAG}_prof_passA.log 2>&1; tail -1 $O/${TAG}_prof_passA.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_grad|k_flux|k_gather|k_tpb" -s 0 -c 1 -o $O/${TAG}_prof_ax python tools/prof_run.py --N 4 --ax 1 --pcg 0 > $O/${TAG}_prof_ax.log 2>&1; tail -1 $O/${TAG}_prof_ax.log

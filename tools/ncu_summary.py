@@ -74,14 +74,14 @@ def main():
             f.write("- %s %s: %s\n" % (d["id"], d["kernel"][:40], ", ".join("%s %.1f" % kv for kv in d["stall_pct"].items())))
     def kname(d):
         return d["kernel"].split("<")[0].split()[-1].split("::")[-1]
-    pa = [d for d in out if ("<%d, 1" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe")]
+    pa = [d for d in out if ("<%d, 1" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe", "k_tpb", "k_gather")]
     summ_path = os.path.join(os.path.dirname(a.out), "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     if pa:
         summ["pass_a"] = {"N": a.N, "K": a.K, "kernel": kname(pa[0]), "dram_bytes_per_launch": pa[0].get("dram_bytes"),
                           "duration_us_under_ncu": pa[0].get("duration_us"), "source": os.path.basename(a.rep),
                           "pcg_iteration": a.iteration}
-    ax = [d for d in out if ("<%d, 0" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe")]
+    ax = [d for d in out if ("<%d, 0" % a.N) in d["kernel"] and kname(d) in ("k_sipdg", "k_pipe", "k_tpb", "k_gather")]
     if ax:
         summ["ax"] = {"N": a.N, "K": a.K, "kernel": kname(ax[0]), "dram_bytes_per_launch": ax[0].get("dram_bytes"),
                       "duration_us_under_ncu": ax[0].get("duration_us"), "source": os.path.basename(a.rep)}
