@@ -101,7 +101,7 @@ def chebyshev(A, dinv, b, lmax, steps=2, a=None):
 
 
 class PMG:
-    """The hierarchy of R22-R25 for one mesh and fine degree N (lambda: the screening coefficient of
+    """The hierarchy of R22-R26 for one mesh and fine degree N (lambda: the screening coefficient of
     A = -L + lambda, the same on every level)."""
 
     def __init__(self, VX, VY, EToV, bc, N, lam=0.0):

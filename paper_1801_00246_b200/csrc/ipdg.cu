@@ -867,7 +867,7 @@ static int capture(ipdg_ctx c, int iters, cudaGraphExec_t* out) {
   return IPDG_OK;
 }
 
-// ---- p-multigrid preconditioner (IPDG_PRECOND_PMG; pmg.cuh, oracle/pmg.py, R22-R25)
+// ---- p-multigrid preconditioner (IPDG_PRECOND_PMG; pmg.cuh, oracle/pmg.py, R22-R26)
 static int level_ax(ipdg_ctx c, int l, const double* u, double* Au, cudaStream_t s) {
   ipdg_ctx lc = l == 0 ? c : c->pmg[l].ctx;
   DISPATCH(lc->N, ax(lc, u, Au, c->pmg_lambda, s));

@@ -1,4 +1,4 @@
-"""Pins of the p-multigrid oracle (oracle/pmg.py, R22-R25).
+"""Pins of the p-multigrid oracle (oracle/pmg.py, R22-R26).
 
 Each pin checks a piece against something other than the oracle's own formula: the coarsening schedule
 against SPEC's worked example, interpolation against closed-form monomials, the restriction against an
