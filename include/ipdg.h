@@ -141,6 +141,15 @@ int ipdg_pcg_end(ipdg_ctx ctx, ipdg_stats* stats, void* stream);
  * direction update + Ax + p.Ap) and pass B (residual update + dots).  Synchronizes. */
 int ipdg_pcg_iterate_profiled(ipdg_ctx ctx, int64_t n, double* ms_pass_a, double* ms_pass_b, void* stream);
 
+/* Subcycling advection operator (NEXT-4; Eq. INS_CUB_N, Eq. KSS_3, Alg. SSV / SSS):
+ * (Nu, Nv) = N~(U_bar, U~) for the advective velocity (ub, vb) and the advected field (ut, vt), device
+ * vectors K x Np each, nodal output (the (J M)^{-1} of the weak form applied).  Cubature exact to degree
+ * 3N (volume: collapsed Gauss-Legendre; faces: Gauss-Legendre), local Lax-Friedrichs flux with
+ * Lambda = max |n.U_bar+-| and Alg. SSS's dissipative sign (R27); boundary traces by the
+ * velocity mirrors of the face codes (R28: code 1 U+ = U-, code 2 U+ = -U-).  One partition only. */
+int ipdg_advect(ipdg_ctx ctx, const double* ub, const double* vb, const double* ut, const double* vt, double* Nu,
+                double* Nv, void* stream);
+
 /* One p-multigrid V-cycle z = B r (IPDG_PRECOND_PMG's preconditioner, R22-R26),
  * device vectors K x Np, builds the level hierarchy for `lambda` on first use (child contexts of
  * degrees N/2, ..., 1 on the same mesh, their diagonals and power-iteration lmax).  Async on `stream`

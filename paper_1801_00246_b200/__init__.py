@@ -226,6 +226,13 @@ class Ipdg:
         check(lib().ipdg_pmg_apply(self.ctx, _ptr(r), _ptr(z), float(lam), _stream(stream)), self.ctx)
         return z
 
+    def advect(self, ub, vb, ut, vt, stream=None):
+        """Subcycling advection operator (Nu, Nv) = N~(U_bar, U~) (ipdg_advect, NEXT-4)."""
+        Nu, Nv = self._empty(), self._empty()
+        check(lib().ipdg_advect(self.ctx, _ptr(ub), _ptr(vb), _ptr(ut), _ptr(vt), _ptr(Nu), _ptr(Nv),
+                                _stream(stream)), self.ctx)
+        return Nu, Nv
+
     def pmg_info(self):
         deg = (ctypes.c_int * 16)()
         lm = (ctypes.c_double * 16)()

@@ -52,6 +52,7 @@ SIGNATURES = {
     "ipdg_pcg_solve_host": (_int, [_vp, _vp, _vp, _d, _int, _d, _i64, _c.POINTER(ipdg_stats), _vp]),
     "ipdg_comm_init": (_int, [_vp, _vp, _int, _int]),
     "ipdg_pmg_apply": (_int, [_vp, _vp, _vp, _d, _vp]),
+    "ipdg_advect": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ipdg_pmg_info": (_int, [_vp, _vp, _vp, _int]),
     "ipdg_loopback_pcg_solve": (_int, [_vp, _int, _vp, _vp, _d, _int, _d, _i64, _c.POINTER(ipdg_stats), _vp]),
     "ipdg_upload_halo": (_int, [_vp, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp]),

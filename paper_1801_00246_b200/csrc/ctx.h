@@ -70,6 +70,7 @@ struct ipdg_ctx_s {
   PcgState* pmg_gate = nullptr;   // PCG state that gates the cycle's vector kernels (null: ipdg_pmg_apply)
   std::vector<int32_t> pend_etov;  // mesh kept for the child contexts
   double tau_scale = 1.0;
+  double* adv_tab = nullptr;  // advection operators I | Pr | Ps | If | Lc (build_advect_ops), built on first use
   int grid_cap = 0;  // debug: cap on every persistent grid (0 = off)
   int variant = 0;  // 0 auto, 1 fused, 2 split, 3 thread-per-element (N <= 4), 4 pipelined fused
   // pipelined fused variant (k_pipe): same schedule as k_sipdg; grid 0 = does not fit
@@ -187,5 +188,6 @@ struct ImplOps {
   int (*diag)(ipdg_ctx, double*, double, cudaStream_t);
   int (*mass)(ipdg_ctx, const double*, double*, cudaStream_t);
   int (*upload_constants)(ipdg_ctx);
+  int (*advect)(ipdg_ctx, const double* const*, double* const*, cudaStream_t);
 };
 const ImplOps* impl_ops(int N);

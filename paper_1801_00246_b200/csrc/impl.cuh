@@ -12,6 +12,7 @@
 #include "sipdg_gather.cuh"
 #include "dgops.cuh"
 #include "sipdg_tpb.cuh"
+#include "advect.cuh"
 
 #ifndef IPDG_TPB_MAXN
 #define IPDG_TPB_MAXN 8  // highest degree with a k_tpb instantiation (lower it for quick rebuilds)
@@ -661,6 +662,44 @@ struct Impl {
     return IPDG_OK;
   }
 
+  // subcycling advection operator (NEXT-4, advect.cuh): fields = ub, vb, ut, vt; out = Nu, Nv
+  static int advect(ipdg_ctx c, const double* const* fields, double* const* out, cudaStream_t s) {
+    using A = TrA<N>;
+    if (!c->adv_tab) {
+      const AdvectOps ops = build_advect_ops(c->ref);
+      if (ops.nc != A::NC || ops.ncf != A::NCF) FAIL(c, IPDG_ECUDA, "advection cubature size mismatch");
+      std::vector<double> t(ops.I);
+      t.insert(t.end(), ops.Pr.begin(), ops.Pr.end());
+      t.insert(t.end(), ops.Ps.begin(), ops.Ps.end());
+      t.insert(t.end(), ops.If.begin(), ops.If.end());
+      t.insert(t.end(), ops.Lc.begin(), ops.Lc.end());
+      TRY(upload(c, &c->adv_tab, t.data(), t.size()));
+      const size_t bytes = (size_t)A::TOTAL * sizeof(double);
+      CUDA_TRY(c, cudaFuncSetAttribute(k_advect<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    }
+    AdvectArgs a;
+    a.K = c->K;
+    a.geo = c->geo;
+    a.gG = c->gG;
+    a.nbg = c->nbg;
+    a.I = c->adv_tab;
+    a.Pr = a.I + A::NC * A::NP;
+    a.Ps = a.Pr + A::NP * A::NC;
+    a.If = a.Ps + A::NP * A::NC;
+    a.Lc = a.If + A::NCF * A::NFP;
+    a.ub = fields[0];
+    a.vb = fields[1];
+    a.ut = fields[2];
+    a.vt = fields[3];
+    a.Nu = out[0];
+    a.Nv = out[1];
+    const int grid = (int)((c->K + A::EB - 1) / A::EB);
+    k_advect<N><<<grid, A::NTHR, (size_t)A::TOTAL * sizeof(double), s>>>(a);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return IPDG_OK;
+  }
+
   static int diag(ipdg_ctx c, double* d, double lambda, cudaStream_t s) {
     const int64_t n = c->K * T::NP;
     k_diag<N><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, c->geo, c->etoe, c->bcode, c->diagtab, c->tau_c, lambda, d);
@@ -683,6 +722,6 @@ struct Impl {
     static const ImplOps ops = {Impl<N_>::build_tables, Impl<N_>::build_diagtab, Impl<N_>::configure,         \
                                 Impl<N_>::resolve,      Impl<N_>::ax,            Impl<N_>::pass_a,            \
                                 Impl<N_>::pass_b_bj,    Impl<N_>::dgop,          Impl<N_>::diag, Impl<N_>::mass,              \
-                                Impl<N_>::upload_constants}; \
+                                Impl<N_>::upload_constants, Impl<N_>::advect}; \
     return &ops;                                                                                               \
   }

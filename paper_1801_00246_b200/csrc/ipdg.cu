@@ -99,10 +99,11 @@ static void free_mesh(ipdg_ctx c) {
   c->hostio = nullptr;
   c->hostio_n = 0;
   void* ptrs[] = {c->geo, c->gG, c->gF, c->nbr, c->goff, c->gid, c->boff, c->etoe, c->bcode, c->vxy, c->nbg, c->W2,
-                  c->nbt, c->gfoff_t, c->gface_t, c->tauF, c->blist_t};
+                  c->nbt, c->gfoff_t, c->gface_t, c->tauF, c->blist_t, c->adv_tab};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->nbt = nullptr; c->gfoff_t = nullptr; c->gface_t = nullptr; c->tauF = nullptr; c->blist_t = nullptr;
+  c->adv_tab = nullptr;
   c->nblocks_t = 0; c->gmax_t = 0;
   c->geo = nullptr; c->gG = nullptr; c->gF = nullptr; c->nbr = nullptr; c->goff = nullptr; c->gid = nullptr; c->boff = nullptr; c->etoe = nullptr;
   c->nbg = nullptr; c->W2 = nullptr;
@@ -1403,6 +1404,18 @@ int ipdg_loopback_pcg_solve(ipdg_ctx* cs, int P, const double* const* b, double*
   if (stats)
     for (int p = 0; p < P; ++p) stats[p].seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return rc;
+}
+
+int ipdg_advect(ipdg_ctx c, const double* ub, const double* vb, const double* ut, const double* vt, double* Nu, double* Nv,
+                void* stream) {
+  if (!c || !ub || !vb || !ut || !vt || !Nu || !Nv || Nu == Nv) return IPDG_EINVAL;
+  for (const double* in : {ub, vb, ut, vt})
+    if (in == Nu || in == Nv) FAIL(c, IPDG_EINVAL, "ipdg_advect: outputs must not alias the inputs");
+  if (c->K == 0) FAIL(c, IPDG_ESTATE, "ipdg_advect before ipdg_upload_mesh");
+  if (c->H > 0 || c->S > 0) FAIL(c, IPDG_ESTATE, "ipdg_advect: partitioned meshes are not supported");
+  const double* f[4] = {ub, vb, ut, vt};
+  double* o[2] = {Nu, Nv};
+  DISPATCH(c->N, advect(c, f, o, (cudaStream_t)stream));
 }
 
 int ipdg_pmg_apply(ipdg_ctx c, const double* r, double* z, double lambda, void* stream) {

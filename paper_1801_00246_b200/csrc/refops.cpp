@@ -241,4 +241,92 @@ std::vector<double> interp_matrix(const RefOps& F, const RefOps& Cr) {
   return matmul(Vfc, invert(Vc, nc), nf, nc, nc);
 }
 
+namespace {
+// Gauss-Legendre rule on [-1, 1] (Newton on the three-term recurrence of P_n, Chebyshev start)
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double t = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = t;
+      for (int k = 1; k < n; ++k) {
+        const double p2 = ((2 * k + 1) * t * p1 - k * p0) / (k + 1);
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (t * p1 - p0) / (t * t - 1.0);
+      const double dt = p1 / dp;
+      t -= dt;
+      if (std::fabs(dt) < 1e-16) break;
+    }
+    x[n - 1 - i] = t;
+    w[n - 1 - i] = 2.0 / ((1.0 - t * t) * dp * dp);
+  }
+}
+}  // namespace
+
+AdvectOps build_advect_ops(const RefOps& R) {
+  const int N = R.N, Np = R.Np, Nfp = R.Nfp;
+  const int n = (3 * N + 2) / 2 + 1;  // 2n - 1 >= 3N + 1 (the Duffy factor adds one degree in b)
+  AdvectOps A;
+  std::vector<double> g, gw;
+  gauss_legendre(n, g, gw);
+  A.nc = n * n;
+  A.ncf = n;
+  std::vector<double> rc(A.nc), sc(A.nc), wc(A.nc);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double a = g[i], b = g[j];
+      rc[i * n + j] = 0.5 * (1 + a) * (1 - b) - 1.0;
+      sc[i * n + j] = b;
+      wc[i * n + j] = gw[i] * gw[j] * 0.5 * (1 - b);
+    }
+  // Vandermonde of the nodes and of the cubature points (value and gradients)
+  std::vector<double> V(Np * Np), Vc(A.nc * Np), Vcr(A.nc * Np), Vcs(A.nc * Np);
+  for (int q = 0; q < Np; ++q) {
+    int k = 0;
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j, ++k) psi(i, j, R.r[q], R.s[q], &V[q * Np + k], nullptr, nullptr);
+  }
+  for (int q = 0; q < A.nc; ++q) {
+    int k = 0;
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j, ++k) psi(i, j, rc[q], sc[q], &Vc[q * Np + k], &Vcr[q * Np + k], &Vcs[q * Np + k]);
+  }
+  const std::vector<double> Vinv = invert(V, Np);
+  A.I = matmul(Vc, Vinv, A.nc, Np, Np);                 // nc x Np
+  const std::vector<double> Dcr = matmul(Vcr, Vinv, A.nc, Np, Np), Dcs = matmul(Vcs, Vinv, A.nc, Np, Np);
+  const std::vector<double> Minv = R.Minv;             // M^{-1} = V V^T
+  A.Pr.assign(Np * A.nc, 0.0);
+  A.Ps.assign(Np * A.nc, 0.0);
+  for (int nn = 0; nn < Np; ++nn)
+    for (int q = 0; q < A.nc; ++q) {
+      double pr = 0, ps = 0;
+      for (int m = 0; m < Np; ++m) {
+        pr += Minv[nn * Np + m] * Dcr[q * Np + m];
+        ps += Minv[nn * Np + m] * Dcs[q * Np + m];
+      }
+      A.Pr[nn * A.nc + q] = pr * wc[q];
+      A.Ps[nn * A.nc + q] = ps * wc[q];
+    }
+  // face points: Lagrange basis of the Nfp GLL face nodes (face parameter xi in face node order)
+  std::vector<double> V1(Nfp * Nfp), V1g(n * Nfp);
+  for (int a = 0; a < Nfp; ++a)
+    for (int k = 0; k < Nfp; ++k) V1[a * Nfp + k] = jacobiP(R.gll[a], 0, 0, k);
+  for (int a = 0; a < n; ++a)
+    for (int k = 0; k < Nfp; ++k) V1g[a * Nfp + k] = jacobiP(g[a], 0, 0, k);
+  A.If = matmul(V1g, invert(V1, Nfp), n, Nfp, Nfp);
+  A.Lc.assign(Np * 3 * n, 0.0);
+  for (int nn = 0; nn < Np; ++nn)
+    for (int f = 0; f < 3; ++f)
+      for (int j = 0; j < n; ++j) {
+        double v = 0;
+        for (int k = 0; k < Nfp; ++k) v += Minv[nn * Np + R.Fmask[f * Nfp + k]] * A.If[j * Nfp + k];
+        A.Lc[nn * 3 * n + f * n + j] = v * gw[j];
+      }
+  return A;
+}
+
 }  // namespace ipdg

@@ -22,4 +22,16 @@ RefOps build_refops(int N);
 // the degree-fine nodes, V_c(r_f, s_f) V_c^{-1}
 std::vector<double> interp_matrix(const RefOps& fine, const RefOps& coarse);
 
+// Subcycling advection operators (Eq. INS_CUB_N; Alg. SSV / SSS):
+// volume cubature = Gauss-Legendre x Gauss-Legendre on the collapsed square with the Duffy factor in the
+// weights, face cubature = Gauss-Legendre, both exact to degree 3N.
+struct AdvectOps {
+  int nc = 0, ncf = 0;               // volume points, points per face
+  std::vector<double> I;             // nc x Np: nodal basis at the volume points
+  std::vector<double> Pr, Ps;        // Np x nc: M^{-1} w_i (d l_m / dr)(x_i), likewise d/ds
+  std::vector<double> If;            // ncf x Nfp: face-node Lagrange basis at the face points (face order)
+  std::vector<double> Lc;            // Np x 3 ncf: M^{-1} w_j l_m(x_fj) (cubature lift)
+};
+AdvectOps build_advect_ops(const RefOps& R);
+
 }  // namespace ipdg
