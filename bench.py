@@ -503,6 +503,36 @@ def run_next(args):
                               "us": round(1e3 * ms, 2), "gdofs": round(K * Np / (ms / 1e3) / 1e9, 2),
                               "hbm_gbs_algorithmic": round(byt / (ms / 1e3) / 1e9, 1),
                               "hbm_frac": round(byt / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)}), flush=True)
+        # NEXT-3: p-multigrid V-cycle (one application) and NEXT-4: subcycling advection operator
+        r = torch.rand(K, Np, dtype=torch.float64, device="cuda")
+        op.pmg_apply(r)
+        nq = (3 * N + 2) // 2 + 1
+        nc, ncf, nfp = nq * nq, nq, N + 1
+        adv_flop = 2 * (4 * nc * Np + 8 * nc * Np + 3 * ncf * nfp * 8 + 2 * Np * 3 * ncf)  # per element (MACs x 2)
+        fl = [torch.rand(K, Np, dtype=torch.float64, device="cuda") for _ in range(4)]
+        for name, fn in (("NEXT-3 p-multigrid V-cycle", lambda: op.pmg_apply(r)),
+                         ("NEXT-4 subcycling advection N~(U_bar, U~)", lambda: op.advect(*fl))):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(20):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 20
+            line = {"next": name, "config": "C2 mesh", "N": N, "K": K, "us": round(1e3 * ms, 2),
+                    "gdofs": round(K * Np / (ms / 1e3) / 1e9, 2)}
+            if name.startswith("NEXT-4"):
+                byt = (8 * Np * 6 + 48) * K
+                line.update({"fp64_tflops": round(adv_flop * K / (ms / 1e3) / 1e12, 2),
+                             "fp64_frac": round(adv_flop * K / (ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                             "hbm_gbs_algorithmic": round(byt / (ms / 1e3) / 1e9, 1), "bound": "fp64",
+                             "flop_per_elem": adv_flop})
+            else:
+                line["levels"] = [[d, round(l, 4)] for d, l in op.pmg_info()]
+            print(json.dumps(line), flush=True)
         del op
         torch.cuda.empty_cache()
 
