@@ -668,9 +668,16 @@ struct Impl {
     if (!c->adv_tab) {
       const AdvectOps ops = build_advect_ops(c->ref);
       if (ops.nc != A::NC || ops.ncf != A::NCF) FAIL(c, IPDG_ECUDA, "advection cubature size mismatch");
-      std::vector<double> t(ops.I);
-      t.insert(t.end(), ops.Pr.begin(), ops.Pr.end());
-      t.insert(t.end(), ops.Ps.begin(), ops.Ps.end());
+      // transposed layouts (coalesced across the threads of k_advect): IT [NP][NC], PrT / PsT [NC][NP]
+      std::vector<double> t(A::NP * A::NC), pr(A::NC * A::NP), ps(A::NC * A::NP);
+      for (int q = 0; q < A::NC; ++q)
+        for (int j = 0; j < A::NP; ++j) {
+          t[j * A::NC + q] = ops.I[q * A::NP + j];
+          pr[q * A::NP + j] = ops.Pr[j * A::NC + q];
+          ps[q * A::NP + j] = ops.Ps[j * A::NC + q];
+        }
+      t.insert(t.end(), pr.begin(), pr.end());
+      t.insert(t.end(), ps.begin(), ps.end());
       t.insert(t.end(), ops.If.begin(), ops.If.end());
       t.insert(t.end(), ops.Lc.begin(), ops.Lc.end());
       TRY(upload(c, &c->adv_tab, t.data(), t.size()));
@@ -682,10 +689,10 @@ struct Impl {
     a.geo = c->geo;
     a.gG = c->gG;
     a.nbg = c->nbg;
-    a.I = c->adv_tab;
-    a.Pr = a.I + A::NC * A::NP;
-    a.Ps = a.Pr + A::NP * A::NC;
-    a.If = a.Ps + A::NP * A::NC;
+    a.IT = c->adv_tab;
+    a.PrT = a.IT + A::NC * A::NP;
+    a.PsT = a.PrT + A::NP * A::NC;
+    a.If = a.PsT + A::NP * A::NC;
     a.Lc = a.If + A::NCF * A::NFP;
     a.ub = fields[0];
     a.vb = fields[1];
