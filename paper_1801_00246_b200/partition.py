@@ -67,14 +67,37 @@ def global_connectivity(EToV):
     return EToE.reshape(K, 3), EToF.reshape(K, 3)
 
 
+def local_connectivity(EToV, part, r):
+    """EToE, EToF for the rows of rank r's elements only (global element ids), without sorting the whole
+    mesh: the candidates are the elements that share a vertex with rank r (every face neighbour shares
+    two), and only own + candidates are keyed and sorted.  Returns (elems, EToE_r, EToF_r)."""
+    elems = np.nonzero(part == r)[0]
+    verts = np.unique(EToV[elems])
+    touch = np.isin(EToV, verts).any(axis=1)
+    touch[elems] = False
+    sub = np.concatenate([elems, np.nonzero(touch)[0]])
+    E, F = global_connectivity(EToV[sub])
+    Eo, Fo = E[:elems.size], F[:elems.size]
+    Eg = np.where(Eo >= 0, sub[np.maximum(Eo, 0)], -1)
+    return elems, Eg, Fo
+
+
 def split(mesh, part, nparts, ranks=None):
-    """List of RankMesh, one per rank (or only for `ranks`)."""
+    """List of RankMesh, one per rank (or only for `ranks`: then each rank's face connectivity is built
+    from its own elements and their vertex neighbours, not from a sort of the whole mesh)."""
     EToV = np.asarray(mesh["EToV"])
     bc = np.asarray(mesh["bc"])
     part = np.asarray(part)
-    EToE, EToF = global_connectivity(EToV)
+    local = ranks is not None
+    if not local:
+        EToE, EToF = global_connectivity(EToV)
     out = []
     for r in (range(nparts) if ranks is None else ranks):
+        if local:
+            elems_l, E_l, F_l = local_connectivity(EToV, part, r)
+            EToE = np.full((EToV.shape[0], 3), -1, dtype=np.int64)
+            EToF = np.full((EToV.shape[0], 3), -1, dtype=np.int64)
+            EToE[elems_l], EToF[elems_l] = E_l, F_l
         elems = np.nonzero(part == r)[0]
         g2l = -np.ones(EToV.shape[0], dtype=np.int64)
         g2l[elems] = np.arange(elems.size)

@@ -153,3 +153,19 @@ def test_gloo_world2_partitioned_operator_and_pcg():
         assert np.abs(Au_local - Au[elems]).max() <= 1e-12 * np.abs(Au).max()
         assert abs(it - st["iterations"]) <= 1
         assert np.abs(x - xg[elems]).max() <= 1e-8 * np.abs(xg).max()
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_rank_local_split_equals_global_split(P):
+    """partition.split(..., ranks=[r]) builds rank r's connectivity from its own elements and their vertex
+    neighbours only (no sort of the whole mesh); the plans must be identical to the global construction."""
+    m = meshgen.square(15, jitter=0.2, diag="random", order="morton", seed=9,
+                       tag=lambda x, y: np.where(y > 0.5, 1, 2).astype(np.int8))
+    part = meshgen.rcb_partition(m["VX"], m["VY"], m["EToV"], P)
+    full = partition.split(m, part, P)
+    for r in range(P):
+        loc = partition.split(m, part, P, ranks=[r])[0]
+        ref = full[r]
+        for name in ("elems", "EToV", "bc", "remote", "remote_face", "ghosts", "nbr_ranks", "send_off",
+                     "send_elems", "recv_off"):
+            assert np.array_equal(getattr(loc, name), getattr(ref, name)), (P, r, name)
