@@ -244,13 +244,13 @@ def cpu_oracle_sample(N, iters, nx):
 
 
 # ---------------------------------------------------------------- our arm
-def _solve(op, b, xs, stream, world, dev):
+def _solve(op, b, xs, stream, world, dev, precond=1):
     import torch
     torch.cuda.synchronize()
     barrier(world)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
-    _, sst = op.pcg_solve(b, xs, precond=1, tol=1e-8, maxit=_solve.maxit)
+    _, sst = op.pcg_solve(b, xs, precond=precond, tol=1e-8, maxit=_solve.maxit)
     s1.record(stream)
     torch.cuda.synchronize()
     return max_over_ranks(s0.elapsed_time(s1), world, dev), sst
@@ -338,8 +338,15 @@ def run_ours(args):
     # one full Jacobi-PCG solve to 1e-8 (solves/s)
     solve_ms, sst = float("nan"), {"iterations": None, "rel_residual": None}
     xs = torch.zeros_like(b)
+    pmg = None
     if not args.no_solve:
         solve_ms, sst = _solve(op, b, xs, stream, world, dev)
+        if world == 1:  # NEXT-3: the same solve with the p-multigrid preconditioner (hierarchy built first)
+            op.pcg_solve(b, torch.zeros_like(b), precond=3, tol=1e-8, maxit=1)
+            pms, pst = _solve(op, b, torch.zeros_like(b), stream, world, dev, precond=3)
+            pmg = {"tol": 1e-8, "iterations": pst["iterations"], "ms": round(pms, 3), "solves_per_s": round(1e3 / pms, 3),
+                   "rel_residual": pst["rel_residual"], "levels": [d for d, _ in op.pmg_info()],
+                   "note": "IPDG_PRECOND_PMG (DESIGN.md R22-R26); setup (hierarchy, graphs) excluded"}
     # e2e through the public API with host buffers, the call a user makes: ipdg_pcg_solve_host copies b and
     # x0 from pinned host memory, solves to 1e-8 and copies x back.  One untimed call first (the library
     # allocates its per-context staging buffers and captures the iteration graphs once per mesh).
@@ -394,6 +401,7 @@ def run_ours(args):
         "ax_only": {"gdofs": round(ax_gdofs, 3), "ms": round(ax_ms, 5), "buffers_rotated": nbuf},
         "pcg_solve": {"tol": 1e-8, "iterations": sst["iterations"], "ms": (round(solve_ms, 3) if solve_ms == solve_ms else None),
                       "solves_per_s": (round(1e3 / solve_ms, 3) if solve_ms == solve_ms else None), "rel_residual": sst["rel_residual"]},
+        "pcg_solve_pmg": pmg,
         "kernel_config": info,
     }
     if rank == 0:
