@@ -55,6 +55,7 @@ struct ipdg_ctx_s {
   int nbt_split[2] = {0, 0};
   size_t smem_tpb_m[2] = {0, 0};  // [mode]
   bool tpb_ok[2][2] = {{false, false}, {false, false}};  // [mode][lam] fits on an SM
+  int tpb_grid[2][2] = {{0, 0}, {0, 0}};  // [mode][lam] persistent grid: resident CTAs per SM x SMs
   // p-multigrid preconditioner (IPDG_PRECOND_PMG; pmg.cuh, R22-R25): level 0 is this context,
   // levels 1.. are child contexts of degree d_l on the same mesh
   struct PmgLevel {

@@ -221,6 +221,14 @@ struct Impl {
         int occ = 0;
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TrB<N>::NTHR, bytes));
         c->tpb_ok[mode][lam] = occ > 0;
+        // persistent pass A (profiles/r02b_tpb_experiments.txt); IPDG_TPB_PERSIST=0 (measurement): one CTA
+        // per block
+        const char* ev = getenv("IPDG_TPB_PERSIST");
+        const bool persist = ev ? atoi(ev) != 0 : true;
+        // IPDG_TPB_CTAS=k (measurement): at most k resident CTAs per SM in the persistent grid
+        const char* ek = getenv("IPDG_TPB_CTAS");
+        const int cps = (ek && atoi(ek) > 0) ? std::min(std::max(1, occ), atoi(ek)) : std::max(1, occ);
+        c->tpb_grid[mode][lam] = persist ? cps * c->sms : (1 << 30);
       }
     }
     return IPDG_OK;
@@ -228,7 +236,7 @@ struct Impl {
 
   // one CTA per block of kTpbE elements (all blocks, or the interior / boundary lists of a split pass A)
   template <int MODE>
-  static int launch_tpb(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s, const int* list, int n) {
+  static int launch_tpb(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s, const int* list, int n, bool comm_slots = false) {
     if constexpr (N > IPDG_TPB_MAXN) {
       FAIL(c, IPDG_EINVAL, "k_tpb not built for N = %d", N);
     } else {
@@ -238,8 +246,14 @@ struct Impl {
     a.tauF = c->tauF;
     a.blist = list;
     a.nlist = n;
-    const int grid = list ? n : c->nblocks_t;
+    int grid = list ? n : c->nblocks_t;
     if (grid <= 0) return IPDG_OK;
+    if (MODE == MODE_PCG_A) {  // Ax: one CTA per block
+      const int pg = c->tpb_grid[1][lam ? 1 : 0];
+      // while a halo exchange is in flight leave a few CTA slots free for NCCL's kernel (as k_pipe)
+      grid = std::min(grid, comm_slots ? std::max(1, std::min(pg, c->sms * 4) - kCommSlots) : pg);
+    }
+    if (MODE == MODE_PCG_A && c->grid_cap > 0) grid = std::min(grid, c->grid_cap);
     if (MODE == MODE_PCG_A && grid > c->partials_cap) FAIL(c, IPDG_ECUDA, "partials buffer too small");
     const size_t smb = c->smem_tpb_m[MODE == MODE_PCG_A ? 1 : 0];
     if (lam) k_tpb<N, MODE, true><<<grid, TrB<N>::NTHR, smb, s>>>(a, c->gmax_t);
@@ -394,7 +408,7 @@ struct Impl {
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : ((mode == 1 && N == 4) ? 4 : 6);
+    if (k == 0) k = (N >= 6) ? 2 : 6;  // profiles/r02b_variants.jsonl
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
     if (k == 6 && !(c->tpb_ok[mode][lam] && (!lam || TrB<N>::HAS_LAM) && (v == nullptr || aligned16(v)))) k = 1;
@@ -582,7 +596,7 @@ struct Impl {
       if (c->split_a) {  // interior blocks, (wait for the halo exchange), halo-boundary blocks
         const int ni = c->nbt_split[0], nbd = c->nbt_split[1];
         a.red_part = (ni > 0 && nbd > 0) ? 1 : 0;
-        if (ni > 0) TRY(launch_tpb<MODE_PCG_A>(c, a, lam, s, c->blist_t, ni));
+        if (ni > 0) TRY(launch_tpb<MODE_PCG_A>(c, a, lam, s, c->blist_t, ni, c->halo_ev_pending));
         if (c->halo_ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_halo, 0));
         a.red_part = (ni > 0 && nbd > 0) ? 2 : 0;
         if (nbd > 0) TRY(launch_tpb<MODE_PCG_A>(c, a, lam, s, c->blist_t + ni, nbd));

@@ -1530,7 +1530,7 @@ int ipdg_info(ipdg_ctx c, int64_t* out, int n) {
   // resolved pass-A kernel for lambda = 0 and its launch shape
   const int kern = [&]() -> int { return impl_ops(c->N)->resolve(c, 1, false, nullptr); }();
   const int64_t ksm = kern == 4 ? (int64_t)c->smem_pipe[1][0] : kern == 6 ? (int64_t)c->smem_tpb_m[1] : (int64_t)c->smem[1][0];
-  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : kern == 6 ? c->nblocks_t : c->grid[1][0];
+  const int64_t kgr = kern == 4 ? c->grid_pipe[1][0] : kern == 6 ? std::min(c->nblocks_t, c->tpb_grid[1][0]) : c->grid[1][0];
   const int64_t v[] = {c->N, c->ref.Np, c->K, c->nblocks, c->E, c->gmax, (int64_t)c->smem[0][0], c->grid[0][0],
                        kern, ksm, kgr};
   for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];

@@ -598,7 +598,11 @@ static __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restr
   const long long k = st->it + 1;
   const double sigma = st->red_A;
   const double rho = st->rho_hist[(k - 1) & 3];
+#ifdef IPDG_DEBUG_NOBREAK  // timing builds of deliberately wrong operators (ablations): alpha = 0, no breakdown
+  if (false) {
+#else
   if (!(sigma > 0.0)) {  // breakdown: p^T A p <= 0 (or NaN)
+#endif
     double v[2] = {0.0, 0.0}, out[2];
     if (grid_reduce<2>(v, red, partials, counter, out)) {
       st->stop_iter = k;
@@ -608,7 +612,11 @@ static __global__ void __launch_bounds__(256) k_pcg_b(int64_t n, double* __restr
     }
     return;
   }
+#ifdef IPDG_DEBUG_NOBREAK
+  const double alpha = 0.0 * (rho / sigma);
+#else
   const double alpha = rho / sigma;
+#endif
   const double* __restrict__ p = (k & 1) ? p_odd : p_even;
   double rz = 0.0, rr = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   const double* C = c_tpb<N>;
   const int tid = threadIdx.x;
   const int64_t K = a.K;
-  const int b = a.blist ? a.blist[blockIdx.x] : (int)blockIdx.x;
 
   PcgDecision d;
   double* pnew = nullptr;
@@ -203,6 +202,35 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   const bool with_x = PCG && d.do_xupd && a.defer_x;
   const double beta = d.beta;
 
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // PCG pass A: persistent CTAs over blocks blockIdx.x, + gridDim.x, ... (of the list for a split pass
+  // A); one grid reduction per CTA at the end, and the CTAs of an SM drift out of phase (one CTA's
+  // staging overlaps another's arithmetic)
+  const int nbl = a.blist ? a.nlist : (int)((K + E - 1) / E);
+  double dot = 0.0;
+  int it = 0;
+  unsigned ph = 0;  // mbarrier phase (flips once per bulk-staged block)
+#ifndef IPDG_TPB_PHASE
+#define IPDG_TPB_PHASE 0  // measurement: clock64 phase durations of two CTAs printed at exit
+#endif
+  long long ph_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_last = 0;
+#define TPB_MARK(k)                                                  \
+  if constexpr (IPDG_TPB_PHASE != 0) {                               \
+    const long long now_ = clock64();                                \
+    if ((k) > 0) ph_acc[(k)] += now_ - ph_last;                      \
+    ph_last = now_;                                                  \
+  }
+  auto block = [&](const int b) {
+  TPB_MARK(0)
+  if (it > 0) {  // the previous block's bulk store has read the rows before they are restaged
+    if (tid == 0) bulk_wait_read();
+    __syncthreads();
+  }
+  TPB_MARK(1)
   const int64_t e0 = (int64_t)b * E;
   const int Eb = (int)min((int64_t)E, K - e0);
   const int64_t g0 = e0 * NP;
@@ -227,11 +255,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
 #pragma unroll
     for (int f = 0; f < 3; ++f) tq3[r][f] = a.tauF[(e0 + sl[r]) * 3 + f];
   }
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
   double* spo = sm + L::FT;              // PCG: p_{k-1} rows
   double* sx = sm + L::FT + E * NP;      // PCG: x rows
   if (bulk) {
@@ -250,12 +273,13 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     }
   }
 
+  TPB_MARK(2)
   // ---- ghost faces, while the bulk copies are in flight: value and trace of the outside neighbour on
   // the shared face, from its row in global memory (L2; PCG: p_k = z + beta p_{k-1}, the owner's FMA)
   // into the ghost-face records (their own region: no ordering against the staging)
   const int gf0 = a.gfoff[b], Gb = a.gfoff[b + 1] - gf0;
 #ifndef IPDG_TPB_SKIP
-#define IPDG_TPB_SKIP 0  // debug: 1 = no ghost pass, 2 = no volume, 4 = no face phase (results wrong)
+#define IPDG_TPB_SKIP 0  // debug: 1 = no ghost pass, 2 = no volume, 4 = no face phase, 8 = no p/x formation (results wrong)
 #endif
   for (int g = tid; g < ((IPDG_TPB_SKIP & 1) ? 0 : Gb); g += NTHR) {
     const int ent = a.gface[gf0 + g];
@@ -279,9 +303,10 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     else ghost_face<N, 2>(un, gq, go);
   }
 
-  if (bulk) mbar_wait(mbar, 0);
+  TPB_MARK(3)
+  if (bulk) { mbar_wait(mbar, ph); ph ^= 1u; }
   else __syncthreads();
-  if (PCG) {  // p_k = z + beta p_{k-1} in place, p_k and the deferred x update x += alpha_{k-1} p_{k-1}
+  if (PCG && !(IPDG_TPB_SKIP & 8)) {  // p_k = z + beta p_{k-1} in place, p_k and the deferred x update x += alpha_{k-1} p_{k-1}
     const double alpha_prev = d.alpha_prev;
 #pragma unroll 4
     for (int q = tid; q < nrow; q += NTHR) {
@@ -292,7 +317,9 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
       if (with_x) a.x[g0 + q] = fma(alpha_prev, po, sx[q]);
     }
   }
+  TPB_MARK(4)
   __syncthreads();  // p_k rows complete; staging consumed before the face records overwrite it
+  TPB_MARK(5)
 
   // ---- own elements (R per thread: slots tid + r NTHR): volume, own face values and traces.  Outer
   // products: NP independent accumulators per element, every constant feeds R FMAs.
@@ -387,7 +414,9 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
       }
   }
   }
+  TPB_MARK(6)
   __syncthreads();  // face records of every slot (own and ghost) visible
+  TPB_MARK(7)
 
   // ---- faces: jump, mirrored boundary traces (R7), flux, lift of the jump, face mass
 #pragma unroll
@@ -483,7 +512,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
     }
   }
   // Au in place over the own rows (phase 2 reads only the face records, never another thread's row)
-  double dot = 0.0;
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (act[r]) {
@@ -501,6 +529,16 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   } else {
     for (int q = tid; q < nrow; q += NTHR) a.Au[g0 + q] = rows[q];
   }
+  TPB_MARK(8)
+  ++it;
+  };  // block
+  // PCG pass A: persistent CTAs (grid = resident CTAs x SMs, IPDG_TPB_PERSIST); Ax: one CTA per block
+  // (the loop costs the Ax instance registers and spills, measured slower)
+  if constexpr (PCG) {
+    for (int bi = blockIdx.x; bi < nbl; bi += gridDim.x) block(a.blist ? a.blist[bi] : bi);
+  } else {
+    block(a.blist ? a.blist[blockIdx.x] : (int)blockIdx.x);
+  }
   if (PCG) {
     double v[1] = {dot}, out[1];
     if (grid_reduce<1>(v, red, a.partials, a.counter, out)) {
@@ -511,7 +549,12 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
       if (d.first) st->bb = d.bbv;
     }
   }
-  if (bulk && tid == 0) bulk_wait_read();  // the bulk store has read the rows before the CTA exits
+  if (tid == 0) bulk_wait_read();  // the last bulk store has read the rows before the CTA exits
+  if constexpr (IPDG_TPB_PHASE != 0) {
+    if (blockIdx.x < 3 && (tid == 0 || tid == 96))
+      printf("TPB_PHASE mode=%d cta=%d tid=%d blocks=%d wait=%lld rec=%lld ghost=%lld mbar_form=%lld bar1=%lld vol=%lld bar2=%lld face_store=%lld\n",
+             MODE, (int)blockIdx.x, tid, it, ph_acc[1], ph_acc[2], ph_acc[3], ph_acc[4], ph_acc[5], ph_acc[6], ph_acc[7], ph_acc[8]);
+  }
 }
 
 }  // namespace ipdg

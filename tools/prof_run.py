@@ -14,6 +14,7 @@ ap.add_argument("--nx", type=int, default=316)
 ap.add_argument("--ax", type=int, default=3)
 ap.add_argument("--pcg", type=int, default=3)
 ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--precond", type=int, default=1)
 a = ap.parse_args()
 mesh = meshgen.square(a.nx, jitter=0.2, diag="random", order="morton", seed=2)
 op = Ipdg(a.N, mesh)
@@ -24,7 +25,7 @@ for _ in range(a.ax):
 if a.pcg:
     b = op.mass(u)
     x = torch.zeros_like(b)
-    op.pcg_begin(b, x, precond=1, tol=0.0)
+    op.pcg_begin(b, x, precond=a.precond, tol=0.0)
     op.pcg_iterate_profiled(a.pcg)
     op.pcg_end()
 torch.cuda.synchronize()
