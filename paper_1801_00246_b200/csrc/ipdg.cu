@@ -882,7 +882,10 @@ static double* lvec(ipdg_ctx c, int l, int which) {  // 0 dinv, 1 b, 2 x, 3 r, 4
 
 // R24 / R26: `steps` Chebyshev steps from x = 0 for A x = b at level l over [a, 1.1 lmax] (smoother: 2 steps,
 // a = lmax / 10; coarsest level: kPmgCoarseSteps, a = 1.1 lmax / kPmgCoarseRatio)
-static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
+// With Ab the right-hand side is the residual b - Ab (stored in the level's r); with acc the last step also
+// adds the result to acc (the V-cycle correction) and, with rdot, reduces rho = rdot . acc into the state.
+static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s, const double* Ab = nullptr,
+                double* acc = nullptr, const double* rdot = nullptr) {
   auto& L = c->pmg[l];
   const bool coarse = (l + 1 == (int)c->pmg.size());
   const int steps = coarse ? kPmgCoarseSteps : 2;
@@ -892,13 +895,17 @@ static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
   double* d = lvec(c, l, 4);
   double* t = lvec(c, l, 5);
   const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
-  k_cheb0<<<g, 256, 0, s>>>(n, b, lvec(c, l, 0), 1.0 / theta, x, d, c->pmg_gate);
+  double* r = lvec(c, l, 3);
+  k_cheb0<<<g, 256, 0, s>>>(n, b, Ab, r, lvec(c, l, 0), 1.0 / theta, x, d, c->pmg_gate);
   c->launches++;
+  const double* bb = Ab ? r : b;
   double rho = 1.0 / sigma;
   for (int m = 1; m < steps; ++m) {
     const double rho_new = 1.0 / (2.0 * sigma - rho);
+    const bool last = (m + 1 == steps);
     TRY(level_ax(c, l, x, t, s));
-    k_cheb1<<<g, 256, 0, s>>>(n, b, t, lvec(c, l, 0), rho_new * rho, 2.0 * rho_new / delta, x, d, c->pmg_gate);
+    k_cheb1<<<g, 256, 0, s>>>(n, bb, t, lvec(c, l, 0), rho_new * rho, 2.0 * rho_new / delta, x, d, last ? acc : nullptr,
+                              last ? rdot : nullptr, c->st, c->partials, c->counter, c->pmg_gate);
     c->launches++;
     rho = rho_new;
   }
@@ -906,29 +913,27 @@ static int cheb(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
   return IPDG_OK;
 }
 
-// R25: x = V_l(b), zero initial guess
-static int vcycle(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s) {
+// R25: x = V_l(b), zero initial guess.  The residuals are formed inside the restriction and the
+// post-smoother's first step, the correction x += y inside its last step (with rdot: and rho = rdot . x).
+// Returns in *dot_done whether rho was reduced (not on a one-level hierarchy).
+static int vcycle(ipdg_ctx c, int l, const double* b, double* x, cudaStream_t s, const double* rdot = nullptr,
+                  bool* dot_done = nullptr) {
   TRY(cheb(c, l, b, x, s));
   if (l + 1 == (int)c->pmg.size()) return IPDG_OK;
   auto& L = c->pmg[l];
   auto& C = c->pmg[l + 1];
   const int64_t n = c->K * L.Np, nc = c->K * C.Np;
-  const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
-  double* r = lvec(c, l, 3);
   double* t = lvec(c, l, 5);
   double* y = lvec(c, l, 6);
   TRY(level_ax(c, l, x, t, s));
-  k_resid<<<g, 256, 0, s>>>(n, b, t, r, c->pmg_gate);
-  k_restrict<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(c->K, L.Np, C.Np, L.I, r, lvec(c, l + 1, 1), c->pmg_gate);
-  c->launches += 2;
+  k_restrict<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(c->K, L.Np, C.Np, L.I, b, t, lvec(c, l + 1, 1), c->pmg_gate);
+  c->launches++;
   TRY(vcycle(c, l + 1, lvec(c, l + 1, 1), lvec(c, l + 1, 2), s));
   k_prolong<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->K, L.Np, C.Np, L.I, lvec(c, l + 1, 2), x, 1, c->pmg_gate);
-  TRY(level_ax(c, l, x, t, s));
-  k_resid<<<g, 256, 0, s>>>(n, b, t, r, c->pmg_gate);
-  c->launches += 2;
-  TRY(cheb(c, l, r, y, s));
-  k_axpy1<<<g, 256, 0, s>>>(n, y, x, c->pmg_gate);
   c->launches++;
+  TRY(level_ax(c, l, x, t, s));
+  TRY(cheb(c, l, b, y, s, t, x, rdot));
+  if (dot_done) *dot_done = rdot != nullptr;
   CUDA_TRY(c, cudaGetLastError());
   return IPDG_OK;
 }
@@ -1012,10 +1017,13 @@ static int pmg_setup(ipdg_ctx c, double lambda, cudaStream_t s) {
 // z = V(r) and rho = r.z -> st->red_B[0] (after the Jacobi-free pass B / init wrote z = r and the norms)
 static int pmg_apply(ipdg_ctx c, cudaStream_t s) {
   c->pmg_gate = c->st;
-  TRY(vcycle(c, 0, c->r, c->zb, s));
-  const int64_t n = c->K * c->ref.Np;
-  k_dot<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(n, c->r, c->zb, nullptr, c->st, c->partials, c->counter);
-  c->launches++;
+  bool dot_done = false;
+  TRY(vcycle(c, 0, c->r, c->zb, s, c->r, &dot_done));
+  if (!dot_done) {  // one-level hierarchy (N = 1): rho = r.z here
+    const int64_t n = c->K * c->ref.Np;
+    k_dot<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(n, c->r, c->zb, nullptr, c->st, c->partials, c->counter);
+    c->launches++;
+  }
   CUDA_TRY(c, cudaGetLastError());
   return IPDG_OK;
 }

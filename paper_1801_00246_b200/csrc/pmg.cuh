@@ -29,55 +29,65 @@ static __global__ void k_prolong(int64_t K, int npf, int npc, const double* __re
   uf[t] = add ? uf[t] + s : s;
 }
 
-// rc = P^T rf element by element: rc[e][j] = sum_i I[i][j] rf[e][i]
+// rc = P^T rf element by element: rc[e][j] = sum_i I[i][j] rf[e][i]; with Af != null the fine residual
+// rf - Af is formed on the fly (the pre-smoothed residual b - A x of the V-cycle, never stored)
 static __global__ void k_restrict(int64_t K, int npf, int npc, const double* __restrict__ I, const double* __restrict__ rf,
-                                  double* __restrict__ rc, const PcgState* gate) {
+                                  const double* __restrict__ Af, double* __restrict__ rc, const PcgState* gate) {
   if (gated(gate)) return;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= K * npc) return;
   const int64_t e = t / npc;
   const int j = (int)(t - e * npc);
   const double* rr = rf + e * npf;
+  const double* ar = Af ? Af + e * npf : nullptr;
   double s = 0.0;
-  for (int i = 0; i < npf; ++i) s = fma(I[i * npc + j], rr[i], s);
+  for (int i = 0; i < npf; ++i) s = fma(I[i * npc + j], ar ? rr[i] - ar[i] : rr[i], s);
   rc[t] = s;
 }
 
-// Chebyshev step 0 from x = 0 (R24): d = D^{-1} b / theta, x = d
-static __global__ void k_cheb0(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv, double inv_theta,
+// Chebyshev step 0 from x = 0 (R24): d = D^{-1} b / theta, x = d.  With Ab != null the right-hand side is
+// the residual b - Ab, formed here and stored in r (the post-smoother of the V-cycle)
+static __global__ void k_cheb0(int64_t n, const double* __restrict__ b, const double* __restrict__ Ab,
+                               double* __restrict__ r, const double* __restrict__ dinv, double inv_theta,
                                double* __restrict__ x, double* __restrict__ d, const PcgState* gate) {
   if (gated(gate)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = dinv[i] * b[i] * inv_theta;
+    double bi = b[i];
+    if (Ab) {
+      bi = bi - Ab[i];
+      r[i] = bi;
+    }
+    const double v = dinv[i] * bi * inv_theta;
     d[i] = v;
     x[i] = v;
   }
 }
 
-// Chebyshev step 1 (R24): d = c1 d + c2 D^{-1} (b - A x), x += d   (Ax = A x, from the level's ipdg Ax)
-static __global__ void k_cheb1(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
+// Chebyshev step 1 (R24): d = c1 d + c2 D^{-1} (b - A x), x += d   (Ax = A x, from the level's ipdg Ax).
+// With acc != null (the post-smoother's last step) also acc += x, the V-cycle's correction of the level
+// iterate; with rdot != null (level 0) the PCG's rho = rdot . acc is reduced into the state (red_B[0])
+static __global__ void __launch_bounds__(256) k_cheb1(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
                                const double* __restrict__ dinv, double c1, double c2, double* __restrict__ x,
-                               double* __restrict__ d, const PcgState* gate) {
+                               double* __restrict__ d, double* __restrict__ acc, const double* __restrict__ rdot,
+                               PcgState* st, double* partials, unsigned int* counter, const PcgState* gate) {
+  __shared__ double red[32 * 3];
   if (gated(gate)) return;
+  double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = fma(c1, d[i], c2 * dinv[i] * (b[i] - Ax[i]));
     d[i] = v;
-    x[i] += v;
+    const double xi = x[i] + v;
+    x[i] = xi;
+    if (acc) {
+      const double ai = acc[i] + xi;
+      acc[i] = ai;
+      if (rdot) s = fma(rdot[i], ai, s);
+    }
   }
-}
-
-// r = b - Ax
-static __global__ void k_resid(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
-                               double* __restrict__ r, const PcgState* gate) {
-  if (gated(gate)) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    r[i] = b[i] - Ax[i];
-}
-
-// x += y
-static __global__ void k_axpy1(int64_t n, const double* __restrict__ y, double* __restrict__ x, const PcgState* gate) {
-  if (gated(gate)) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] += y[i];
+  if (rdot) {
+    double vv[1] = {s}, o[1];
+    if (grid_reduce<1>(vv, red, partials, counter, o)) st->red_B[0] = o[0];
+  }
 }
 
 // deterministic dot product u.v -> out[0] (and, with st, rho = r.z of the PCG state: red_B[0])
