@@ -364,24 +364,6 @@ struct Impl {
         h[B::O_D1DT + m * NFP + k] = D1D[k * NFP + m];
       }
     CUDA_TRY(c, cudaMemcpyToSymbol(c_tpb<N>, h.data(), h.size() * sizeof(double)));
-    if constexpr (B::DMMAV) {  // DMMA B fragments, fragment-major (lane l: row 4 kk + (l & 3), column 8 nt + (l >> 2))
-      constexpr int KS1 = B::KS1, NT1 = B::NT1, KS3 = B::KS3, NT3 = B::NT3, NPN = B::NPN, H = NT1 / 2;
-      std::vector<double> f(B::TABF, 0.0);
-      for (int kk = 0; kk < KS1; ++kk)
-        for (int nt = 0; nt < NT1; ++nt)
-          for (int l = 0; l < 32; ++l) {
-            const int k = 4 * kk + (l & 3), n = 8 * (nt % H) + (l >> 2);  // B[k][n] = Dr[n][k] | Ds[n][k]
-            f[(kk * NT1 + nt) * 32 + l] = (k < NP && n < NP) ? D(nt < H ? R.Dr : R.Ds, n, k) : 0.0;
-          }
-      for (int kk = 0; kk < KS3; ++kk)
-        for (int nt = 0; nt < NT3; ++nt)
-          for (int l = 0; l < 32; ++l) {
-            const int w = 8 * (kk >> 1) + 2 * (l & 3) + (kk & 1);  // W column fed by lane l at k-step kk
-            const int i = w % NPN, n = 8 * nt + (l >> 2);           // S[w][n] = Sr[i][n] | Ss[i][n]
-            f[KS1 * NT1 * 32 + (kk * NT3 + nt) * 32 + l] = (i < NP && n < NP) ? D(w < NPN ? R.Sr : R.Ss, i, n) : 0.0;
-          }
-      CUDA_TRY(c, cudaMemcpyToSymbol(c_tpbf<N>, f.data(), f.size() * sizeof(double)));
-    }
     return IPDG_OK;
   }
 

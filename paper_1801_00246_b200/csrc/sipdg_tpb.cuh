@@ -73,28 +73,10 @@ struct TrB {
 #define IPDG_TPB_UNR 0
 #endif
   static constexpr int UNR = IPDG_TPB_UNR > 0 ? IPDG_TPB_UNR : NP;  // unroll of the row loops (NP: full)
-#ifndef IPDG_TPB_DMMAV
-#define IPDG_TPB_DMMAV 0  // highest degree whose k_tpb volume runs on the FP64 tensor cores (0: none)
-#endif
-  // Volume on DMMA (mma.sync.m8n8k4.f64): per warp, tiles of 8 of its 32 elements,
-  //   P1 [u_r | u_s] = U [Dr^T | Ds^T]   (KS1 k-steps x NT1 n-tiles), chain rule in the C fragments,
-  //   P3 Au_vol = [w_r | w_s] [Sr; Ss]   (KS3 x NT3), A fragments = P1's C fragments (B rows permuted),
-  // operands B from a fragment-major shared copy (one conflict-free LDS.64 per DMMA); the result goes to a
-  // shared row buffer that seeds each thread's face-phase accumulators.  No constant-bank operand per FMA.
-  static constexpr bool DMMAV = (N <= IPDG_TPB_DMMAV) && R == 1 && GRAD;
-  static constexpr int NPK = (NP + 3) / 4 * 4, NPN = (NP + 7) / 8 * 8;
-  static constexpr int KS1 = NPK / 4, NT1 = 2 * NPN / 8, KS3 = 2 * NPN / 4, NT3 = NPN / 8;
-  static constexpr int TABF = DMMAV ? (KS1 * NT1 + KS3 * NT3) * 32 : 0;
-#ifndef IPDG_TPB_DMMA_UNR
-#define IPDG_TPB_DMMA_UNR 1
-#endif
-  static constexpr int DUNR = IPDG_TPB_DMMA_UNR;  // tiles in flight per warp
 };
 
 template <int N>
 __constant__ double c_tpb[TrB<N>::TOTAL];
-template <int N>
-__constant__ double c_tpbf[TrB<N>::TABF > 0 ? TrB<N>::TABF : 1];  // DMMA B fragments (DMMAV)
 
 // shared-memory layout in doubles: rows [E x NP] (+1 pad) | face records ft [E x TS] double2 |
 // ghost-face records gft [gmax x NFP] double2 | mbarrier
@@ -108,10 +90,7 @@ struct TpbLayout {
   static constexpr int FTN = (2 * T::E * T::TS > 2 * T::E * T::NP ? 2 * T::E * T::TS : 2 * T::E * T::NP);
   __host__ __device__ static int gft(int, bool) { return FT + FTN; }
   __host__ __device__ static int mbar(int gmax, bool pcg) { return gft(gmax, pcg) + 2 * gmax * T::NFP; }
-  // DMMAV: B-fragment tables and the volume result rows
-  __host__ __device__ static int tabf(int gmax, bool pcg) { return mbar(gmax, pcg) + 2; }
-  __host__ __device__ static int av(int gmax, bool pcg) { return tabf(gmax, pcg) + T::TABF; }
-  __host__ __device__ static int total(int gmax, bool pcg) { return av(gmax, pcg) + (T::DMMAV ? T::E * T::NP : 0); }
+  __host__ __device__ static int total(int gmax, bool pcg) { return mbar(gmax, pcg) + 2; }
 };
 
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
@@ -223,10 +202,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   const bool with_x = PCG && d.do_xupd && a.defer_x;
   const double beta = d.beta;
 
-  if constexpr (T::DMMAV) {
-    double* tf = sm + L::tabf(gmax, PCG);
-    for (int q = tid; q < T::TABF; q += NTHR) tf[q] = c_tpbf<N>[q];
-  }
   if (tid == 0) {
     mbar_init(mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -355,67 +330,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
 #pragma unroll
     for (int n = 0; n < NP; ++n) Au[r][n] = 0.0;
   if constexpr ((IPDG_TPB_SKIP & 2) != 0) {
-  } else if constexpr (T::DMMAV) {
-    constexpr int KS1 = T::KS1, NT1 = T::NT1, KS3 = T::KS3, NT3 = T::NT3, H = NT1 / 2;
-    const int lane = tid & 31, wbase = tid & ~31, q = lane & 3, mr = lane >> 2;
-    const double* tb1 = sm + L::tabf(gmax, PCG);
-    const double* tb3 = tb1 + KS1 * NT1 * 32;
-    double* AV = sm + L::av(gmax, PCG);
-#pragma unroll(T::DUNR)
-    for (int t = 0; t < 4; ++t) {  // the warp's 32 elements, 8 per tile (E = 128, 4 warps)
-      const int sle = wbase + 8 * t + mr;  // this lane's element slot in the tile
-      const int own = 8 * t + mr;          // lane holding that element's records
-      const double gr = __shfl_sync(0xffffffffu, Grr[0], own);
-      const double gs = __shfl_sync(0xffffffffu, Grs[0], own);
-      const double gt = __shfl_sync(0xffffffffu, Gss[0], own);
-      const double* ur = rows + sle * NP;
-      double c[NT1][2];
-#pragma unroll
-      for (int n = 0; n < NT1; ++n) c[n][0] = c[n][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KS1; ++kk) {
-        const int col = 4 * kk + q;
-        const double av = (col < NP) ? ur[col] : 0.0;
-#pragma unroll
-        for (int n = 0; n < NT1; ++n) dmma(c[n][0], c[n][1], av, tb1[(kk * NT1 + n) * 32 + lane]);
-      }
-      // chain rule (w_r, w_s) = J G (u_r, u_s) and the own traces sJ n.grad u at the face nodes held here
-      double2* fo = ft + sle * TS;
-#pragma unroll
-      for (int n = 0; n < H; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double a_r = c[n][e], a_s = c[n + H][e];
-          const double wr = gr * a_r + gs * a_s, ws = gs * a_r + gt * a_s;
-          c[n][e] = wr;
-          c[n + H][e] = ws;
-          const int i = 8 * n + 2 * q + e;  // node
-          if (i < NP) {
-            const double ui = ur[i];
-#pragma unroll
-            for (int f = 0; f < 3; ++f)
-#pragma unroll
-              for (int k = 0; k < NFP; ++k)
-                if (fmask_cf<N>(f, k) == i) fo[f * NFP + k] = make_double2(ui, f == 0 ? -ws : (f == 1 ? wr + ws : -wr));
-          }
-        }
-      double d[NT3][2];
-#pragma unroll
-      for (int n = 0; n < NT3; ++n) d[n][0] = d[n][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KS3; ++kk) {
-        const double av = c[kk >> 1][kk & 1];  // W column 8 (kk >> 1) + 2 q + (kk & 1) (host-permuted B rows)
-#pragma unroll
-        for (int n = 0; n < NT3; ++n) dmma(d[n][0], d[n][1], av, tb3[(kk * NT3 + n) * 32 + lane]);
-      }
-#pragma unroll
-      for (int n = 0; n < NT3; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = 8 * n + 2 * q + e;
-          if (i < NP) AV[sle * NP + i] = d[n][e];
-        }
-    }
   } else if constexpr (T::GRAD) {
     double wr[R][NP], ws[R][NP];
 #pragma unroll
@@ -503,11 +417,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   TPB_MARK(6)
   __syncthreads();  // face records of every slot (own and ghost) visible
   TPB_MARK(7)
-  if constexpr (T::DMMAV && (IPDG_TPB_SKIP & 2) == 0) {  // this thread's volume result seeds the accumulators
-    const double* AV = sm + L::av(gmax, PCG) + sl[0] * NP;
-#pragma unroll
-    for (int n = 0; n < NP; ++n) Au[0][n] = AV[n];
-  }
 
   // ---- faces: jump, mirrored boundary traces (R7), flux, lift of the jump, face mass
 #pragma unroll
@@ -626,9 +535,6 @@ __global__ void __launch_bounds__(TrB<N>::NTHR, TrB<N>::MINB) k_tpb(AxArgs a, in
   // PCG pass A: persistent CTAs (grid = resident CTAs x SMs, IPDG_TPB_PERSIST); Ax: one CTA per block
   // (the loop costs the Ax instance registers and spills, measured slower)
   if constexpr (PCG) {
-#ifdef IPDG_TPB_STAGGER  // measurement: CTA wave w of the persistent grid starts w x IPDG_TPB_STAGGER ns late
-    if (blockIdx.x >= 148) __nanosleep((unsigned)((blockIdx.x / 148) * IPDG_TPB_STAGGER));
-#endif
     for (int bi = blockIdx.x; bi < nbl; bi += gridDim.x) block(a.blist ? a.blist[bi] : bi);
   } else {
     block(a.blist ? a.blist[blockIdx.x] : (int)blockIdx.x);
