@@ -408,7 +408,9 @@ struct Impl {
   // k_pipe falls back to k_sipdg when it does not fit on an SM or the operand is not 16-byte aligned.
   static int resolve(ipdg_ctx c, int mode, bool lam, const void* v) {
     int k = c->variant;
-    if (k == 0) k = (N >= 6) ? 2 : 6;  // profiles/r02b_variants.jsonl
+    // measured fastest per degree and pass (profiles/r02c_variants.jsonl, r02c_variants_hi.jsonl): k_tpb for
+    // N <= 5; Ax at N = 6 on k_pipe (C3 657 vs 695 us for the split pair), the split pair otherwise
+    if (k == 0) k = (N >= 6) ? ((mode == 0 && N == 6) ? 4 : 2) : 6;
     if (k == 3) k = 1;  // (the thread-per-element variant was retired; it was never the fastest)
     if (k == 5 && N > 4) k = 1;
     if (k == 6 && !(c->tpb_ok[mode][lam] && (!lam || TrB<N>::HAS_LAM) && (v == nullptr || aligned16(v)))) k = 1;

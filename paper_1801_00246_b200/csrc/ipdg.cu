@@ -1060,6 +1060,10 @@ static int pcg_setup(ipdg_ctx c, const double* b, double* x, double lambda, int 
 #define IPDG_TPB_XB 0  // experiment: k_tpb leaves x += alpha p to pass B
 #endif
     c->xb = (kern == 4 && c->pipe_xb[lambda != 0.0]) || (kern == 6 && IPDG_TPB_XB);
+    // the split pass A's W buffer, before any iteration is captured into a graph (the Ax of x0 may run
+    // on another variant, e.g. k_pipe at N = 6, and no longer allocate it)
+    if (kern == 2 && !c->W2)
+      CUDA_TRY(c, cudaMalloc(&c->W2, std::max<int64_t>(1, c->K + c->H) * 2 * c->ref.Np * sizeof(double)));
   }
   PcgState h;
   std::memset(&h, 0, sizeof(h));
