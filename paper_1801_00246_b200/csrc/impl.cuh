@@ -234,7 +234,7 @@ struct Impl {
     return IPDG_OK;
   }
 
-  // one CTA per block of kTpbE elements (all blocks, or the interior / boundary lists of a split pass A)
+  // one CTA per block of tpb_e(N) elements (all blocks, or the interior / boundary lists of a split pass A)
   template <int MODE>
   static int launch_tpb(ipdg_ctx c, AxArgs& a, bool lam, cudaStream_t s, const int* list, int n, bool comm_slots = false) {
     if constexpr (N > IPDG_TPB_MAXN) {

@@ -385,14 +385,14 @@ static int build_block_lists(ipdg_ctx c, int64_t K, const std::vector<int>& boff
   return IPDG_OK;
 }
 
-// k_tpb schedule: blocks of kTpbE consecutive elements (one thread each).  Per own face a slot: the
-// neighbour's position in the block (own element), kTpbE + g for the block's g-th ghost face (neighbour
+// k_tpb schedule: blocks of E = tpb_e(N) consecutive elements (one thread each).  Per own face a slot: the
+// neighbour's position in the block (own element), E + g for the block's g-th ghost face (neighbour
 // outside the block, incl. halo ghosts >= K), or the element itself on a boundary face; flags as nbr.
 // Ghost faces are listed per block as (neighbour << 2) | neighbour's face, sorted by that face so that
 // the recomputation of their traces stays warp-convergent.  The split pass A lists (interior blocks,
 // then blocks with a halo ghost face) follow build_block_lists.
 static int build_tpb(ipdg_ctx c, int64_t K, const std::vector<int>& etoe, const std::vector<int>& etof, const int8_t* bc) {
-  const int E = kTpbE;
+  const int E = tpb_e(c->N);
   const int nb = (int)((K + E - 1) / E);
   std::vector<short4> nbt(K);
   std::vector<int> gfoff(1, 0), gface;

@@ -108,8 +108,8 @@ struct AxArgs {
   struct PcgState* st;
   double* partials;      // [gridDim.x]
   unsigned int* counter;
-  // k_tpb (thread per element, blocks of kTpbE consecutive elements)
-  const short4* nbt;     // [K] per face: slot (own e - e0 < kTpbE, ghost face kTpbE + g, boundary: own) + flags as nbr
+  // k_tpb (thread per element, blocks of tpb_e(N) consecutive elements)
+  const short4* nbt;     // [K] per face: slot (own e - e0 < E, ghost face E + g with E = tpb_e(N), boundary: own) + flags as nbr
   const int* gfoff;      // [nblocks_t + 1] ghost-face list offsets
   const int* gface;      // ghost faces: (neighbour element << 2) | its face, sorted by face within a block
   const double* tauF;    // [K x 3] sJ tau per face
@@ -120,6 +120,10 @@ struct AxArgs {
 #define IPDG_TPB_E 128
 #endif
 constexpr int kTpbE = IPDG_TPB_E;
+// elements per k_tpb block (= threads per CTA) by degree: 256 at N = 4 (two 100 KB CTAs per SM; fewer ghost
+// faces per element; pass A 75.4 vs 77.3 us on C2, profiles/r02d_tpb_block_size.txt), kTpbE elsewhere
+// (N = 5 would not fit twice per SM)
+__host__ __device__ constexpr int tpb_e(int N) { return N == 4 ? 2 * kTpbE : kTpbE; }
 
 // Device-side PCG state (one per context).  See ipdg.cu "PCG protocol".
 struct PcgState {

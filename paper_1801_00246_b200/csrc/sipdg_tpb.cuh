@@ -38,7 +38,7 @@ struct TrB {
   // (the constant path delivers ~8 B/clk/SM: one DFMA per entry caps the FP64 pipe near 50 %,
   // tools/micro_const.cu)
   static constexpr int R = IPDG_TPB_R;
-  static constexpr int E = kTpbE;              // elements per CTA
+  static constexpr int E = tpb_e(N);           // elements per CTA
   static constexpr int NTHR = E / R;
 #ifndef IPDG_TPB_REGS
 #define IPDG_TPB_REGS 0
