@@ -123,7 +123,10 @@ constexpr int kTpbE = IPDG_TPB_E;
 // elements per k_tpb block (= threads per CTA) by degree: 256 at N = 4 (two 100 KB CTAs per SM; fewer ghost
 // faces per element; pass A 75.4 vs 77.3 us on C2, profiles/r02d_tpb_block_size.txt), kTpbE elsewhere
 // (N = 5 would not fit twice per SM)
-__host__ __device__ constexpr int tpb_e(int N) { return N == 4 ? 2 * kTpbE : kTpbE; }
+#ifndef IPDG_TPB_BIGE
+#define IPDG_TPB_BIGE (1 << 4)  // degrees (bit N) with 2 kTpbE-element blocks
+#endif
+__host__ __device__ constexpr int tpb_e(int N) { return ((IPDG_TPB_BIGE >> N) & 1) ? 2 * kTpbE : kTpbE; }
 
 // Device-side PCG state (one per context).  See ipdg.cu "PCG protocol".
 struct PcgState {
